@@ -1,0 +1,101 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+Every comparison is bit-exact (np.array_equal): the oracle restates the
+reference's operations in the same order with the same numpy/scipy calls.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import magnex_oracle as O
+from tests.golden_io import CASES, load, mat_of, packed_of, terms_of
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module", params=CASES)
+def gold(request):
+    z = load(request.param)
+    mat = mat_of(z)
+    spectra = None
+    if bool(z["has_demag"]):
+        packed = packed_of(z)
+        if "packed" in z:
+            assert np.array_equal(packed, z["packed"])
+        assert sha(packed) == str(z["packed_sha"])
+        spectra = O.kernel_spectra(packed)
+        assert sha(spectra) == str(z["spectra_sha"])
+    return request.param, z, mat, terms_of(z, spectra)
+
+
+def test_terms_bit_exact(gold):
+    name, z, mat, terms = gold
+    m0 = z["m0"]
+    plan = O.Plan(mat, terms.mode())
+    if "h_exchange" in z:
+        assert np.array_equal(O.exchange_field(m0, mat, plan), z["h_exchange"])
+    if "h_anisotropy" in z:
+        assert np.array_equal(O.anisotropy_field(m0, mat), z["h_anisotropy"])
+    if "h_dmi" in z:
+        assert np.array_equal(O.dmi_field(m0, mat, plan), z["h_dmi"])
+    if "h_demag" in z:
+        assert np.array_equal(O.demag_field(terms.spectra, m0), z["h_demag"])
+    assert np.array_equal(O.h_eff(0.0, m0, mat, terms, plan), z["h_total"])
+    assert np.array_equal(O.rhs_total(0.0, m0, mat, terms, plan), z["rhs_total"])
+
+
+def test_steps_bit_exact(gold):
+    name, z, mat, terms = gold
+    m0, dt = z["m0"], float(z["dt"])
+    plan = O.Plan(mat, terms.mode())
+
+    def f(t, y):
+        return O.rhs_total(t, y, mat, terms, plan)
+
+    assert np.array_equal(O.rk4_step(m0, 0.0, dt, f, lambda y: O.renormalize(y, mat)),
+                          z["rk4_step"])
+    assert np.array_equal(O.euler_step(m0, 0.0, dt, f), z["euler_step"])
+    e = O.energies(0.0, m0, mat, terms, plan)
+    assert np.array_equal(np.array(e), z["energies"])
+
+
+def test_trace_bit_exact(gold):
+    name, z, mat, terms = gold
+    if "trace_m" not in z:
+        pytest.skip("no trace")
+    n = len(z["trace_t"]) - 1
+    r = O.run(z["m0"], mat, terms, str(z["trace_method"]), float(z["dt"]), max_steps=n,
+              sample_every=1)
+    got = np.array([[row["mx"], row["my"], row["mz"]] for row in r.rows])
+    assert np.array_equal(got, z["trace_m"])
+    assert np.array_equal(np.array([row["t"] for row in r.rows]), z["trace_t"])
+    assert sha(r.m) == str(z["trace_final_sha"])
+
+
+def test_tensor_known_answers():
+    z = load("tensor_known")
+    for i in range(5):
+        cell = z[f"self_{i}_cell"]
+        n6 = O.tensor_elements(1, 1, 1, *cell)[:, 0, 0, 0]
+        full = np.array([[n6[0], n6[1], n6[2]], [n6[1], n6[3], n6[4]], [n6[2], n6[4], n6[5]]])
+        assert np.array_equal(full, z[f"self_{i}"])
+        assert abs(np.trace(full) + 1.0) < 1e-10
+    assert np.array_equal(O.tensor_elements(4, 3, 2, 1e-9, 2e-9, 1.5e-9), z["tensor_432"])
+    assert np.array_equal(O.tensor_elements(120, 1, 1, 1e-9, 1e-9, 1e-9), z["tensor_chain120"])
+
+
+def test_sp4_protocol_trace():
+    """400 RK4 steps of the SP4 field-1 film with energies in the samples."""
+    z = load("sp4_trace")
+    mat = O.make_mat((128, 32, 1), (500e-9 / 128, 125e-9 / 32, 3e-9), 8e5, A=1.3e-11,
+                     alpha=0.02)
+    spectra = O.kernel_spectra(O.packed_tensor(128, 32, 1, 500e-9 / 128, 125e-9 / 32, 3e-9))
+    terms = O.Terms(exchange=True, spectra=spectra, bias=np.array([-19576.0, 3422.0, 0.0]))
+    r = O.run(z["m0"], mat, terms, "rk4", float(z["dt"]), max_steps=400, sample_every=10,
+              with_energies=True)
+    assert np.array_equal(np.array([row["mx"] for row in r.rows]), z["mx"])
+    assert np.array_equal(np.array([row["e_total"] for row in r.rows]), z["e_total"])
+    assert sha(r.m) == str(z["final_sha"])
