@@ -1,0 +1,392 @@
+// Zero-padded FFT demagnetising field (DemagKernel.field, demag.py:203-216).
+//
+// Pipeline for one evaluation (3 components, padded dims p = 2n or 1):
+//   P1  x r2c of the nx real values of every (z,y) row, zero-padded to px,
+//       keeping hx = px/2+1 bins -> X1[z][y][kx][c]      (component-interleaved)
+//   P2  y c2c forward, ny non-zero rows -> py rows       -> X2[z][ky][kx][c]
+//   P3  z c2c forward (nz non-zero) * symmetric 3x3 kernel multiply * z c2c
+//       inverse, keeping the nz rows, in place in X2        (fused, one kernel)
+//   P4  y c2c inverse, keeping the ny rows              -> X1
+//   P5  x c2r of every row, keeping nx values, scaled by 1/(px py pz) -> H
+// A thin film (nz = 1) fuses the y transform with the multiply instead.
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "demag.cuh"
+#include "fft_generic.cuh"
+
+namespace mxb {
+
+static std::vector<int> factorize(int L) {
+    std::vector<int> r;
+    while (L % 8 == 0 && L > 8) { r.push_back(8); L /= 8; }
+    if (L == 8) { r.push_back(8); L = 1; }
+    while (L % 4 == 0) { r.push_back(4); L /= 4; }
+    while (L % 2 == 0) { r.push_back(2); L /= 2; }
+    for (int f = 3; L > 1; f += 2)
+        while (L % f == 0) { r.push_back(f); L /= f; }
+    return r;
+}
+
+int make_plan(int L, int dev, Plan1D* p, double2** tw_owned) {
+    p->L = L;
+    std::vector<int> r = factorize(L);
+    if (r.size() > 24) { set_error("FFT length has too many factors"); return MXB_EINVAL; }
+    p->nst = (int)r.size();
+    for (size_t i = 0; i < r.size(); ++i) p->radix[i] = r[i];
+    std::vector<double2> h(L);
+    for (int n = 0; n < L; ++n) {
+        long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)n / (long double)L;
+        h[n] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    double2* d = nullptr;
+    MXB_CUDA(cudaMalloc(&d, sizeof(double2) * L));
+    MXB_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+    p->tw = d;
+    *tw_owned = d;
+    return MXB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+// P1: rows of real input (line = (row, component), component fastest),
+// zero-padded to L, forward FFT, first hx bins -> out[(row*hxp+kx)*nc + c].
+__global__ void k_rows_r2c(const double* __restrict__ in, long long in_cstride, int in_pitch,
+                           int n_in, double2* __restrict__ out, int hxp, int hx, int nc,
+                           int nrows, Plan1D p, int NL, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 sm[];
+    const int L = p.L, ld = L + 1;
+    double2* a = sm;
+    double2* b = sm + NL * ld;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const long long line0 = (long long)blockIdx.x * NL;
+    const long long nlines = (long long)nrows * nc;
+    for (int u = tid; u < NL * L; u += nthr) {
+        const int l = u / L, e = u - l * L;
+        const long long g = line0 + l;
+        double v = 0.0;
+        if (g < nlines && e < n_in) {
+            const long long row = g / nc;
+            const int c = (int)(g - row * nc);
+            v = in[c * in_cstride + row * in_pitch + e];
+        }
+        a[l * ld + e] = make_double2(v, 0.0);
+    }
+    __syncthreads();
+    double2* r = fft_lines<-1>(a, b, NL, p, tid, nthr);
+    const int rows_here = NL / nc;
+    const long long row0 = line0 / nc;
+    for (int u = tid; u < rows_here * hx * nc; u += nthr) {
+        const int rl = u / (hx * nc), q = u - rl * (hx * nc);
+        const int kx = q / nc, c = q - kx * nc;
+        const long long row = row0 + rl;
+        if (row >= nrows) continue;
+        out[(row * hxp + kx) * nc + c] = r[(rl * nc + c) * ld + kx];
+    }
+}
+
+// P2/P4 (and the kernel-spectrum passes): strided complex lines.
+// line g -> (o = g / Q, q = g % Q); element e at base + e*ES.
+template <int DIR>
+__global__ void k_lines(const double2* in, double2* out, Plan1D p, int n_in, int n_out,
+                        long long ES_in, long long ES_out, int Q, long long nlines,
+                        long long OS_in, long long OS_out, int NL, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 sm[];
+    const int L = p.L, ld = L + 1;
+    double2* a = sm;
+    double2* b = sm + NL * ld;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const long long g0 = (long long)blockIdx.x * NL;
+    for (int u = tid; u < NL * L; u += nthr) {
+        const int l = u % NL, e = u / NL;
+        const long long g = g0 + l;
+        double2 v = make_double2(0.0, 0.0);
+        if (g < nlines && e < n_in) {
+            const long long o = g / Q, q = g - o * Q;
+            v = in[o * OS_in + q + e * ES_in];
+        }
+        a[l * ld + e] = v;
+    }
+    __syncthreads();
+    double2* r = fft_lines<DIR>(a, b, NL, p, tid, nthr);
+    for (int u = tid; u < NL * n_out; u += nthr) {
+        const int l = u % NL, e = u / NL;
+        const long long g = g0 + l;
+        if (g >= nlines) continue;
+        const long long o = g / Q, q = g - o * Q;
+        out[o * OS_out + q + e * ES_out] = r[l * ld + e];
+    }
+}
+
+// P3: forward transform along the outer axis, 3x3 symmetric multiply with
+// the kernel spectra (XX,XY,XZ,YY,YZ,ZZ; demag.py:33-34,211-215), inverse
+// transform, keep n outputs.  In place in X.
+__global__ void k_fused(double2* X, const double2* __restrict__ K, Plan1D p, int n,
+                        long long ES, int hx, int hxp, int G, long long GS, int NK, double scale,
+                        const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 sm[];
+    const int L = p.L, ld = L + 1;
+    const int NL = 3 * NK;
+    double2* a = sm;
+    double2* b = sm + NL * ld;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int g = blockIdx.y;
+    const int kx0 = blockIdx.x * NK;
+    for (int u = tid; u < NL * L; u += nthr) {
+        const int l = u % NL, e = u / NL;
+        const int kx = kx0 + l / 3, c = l % 3;
+        double2 v = make_double2(0.0, 0.0);
+        if (kx < hx && e < n) v = X[g * GS + (long long)kx * 3 + c + e * ES];
+        a[l * ld + e] = v;
+    }
+    __syncthreads();
+    double2* r = fft_lines<-1>(a, b, NL, p, tid, nthr);
+    double2* o = (r == a) ? b : a;
+    for (int u = tid; u < NK * L; u += nthr) {
+        const int kl = u % NK, e = u / NK;
+        const int kx = kx0 + kl;
+        if (kx >= hx) continue;
+        const double2* k6 = K + (((long long)e * G + g) * hxp + kx) * 6;
+        const double2 kxx = k6[0], kxy = k6[1], kxz = k6[2], kyy = k6[3], kyz = k6[4], kzz = k6[5];
+        double2* s0 = r + (3 * kl) * ld + e;
+        const double2 m0 = s0[0], m1 = s0[ld], m2 = s0[2 * ld];
+        double2 h0 = cadd(cadd(cmul(kxx, m0), cmul(kxy, m1)), cmul(kxz, m2));
+        double2 h1 = cadd(cadd(cmul(kxy, m0), cmul(kyy, m1)), cmul(kyz, m2));
+        double2 h2 = cadd(cadd(cmul(kxz, m0), cmul(kyz, m1)), cmul(kzz, m2));
+        s0[0] = make_double2(h0.x * scale, h0.y * scale);
+        s0[ld] = make_double2(h1.x * scale, h1.y * scale);
+        s0[2 * ld] = make_double2(h2.x * scale, h2.y * scale);
+    }
+    __syncthreads();
+    double2* w = fft_lines<1>(r, o, NL, p, tid, nthr);
+    for (int u = tid; u < NL * n; u += nthr) {
+        const int l = u % NL, e = u / NL;
+        const int kx = kx0 + l / 3, c = l % 3;
+        if (kx < hx) X[g * GS + (long long)kx * 3 + c + e * ES] = w[l * ld + e];
+    }
+}
+
+// P5: Hermitian-extend the hx bins to L, inverse FFT, keep n_out real values.
+__global__ void k_rows_c2r(const double2* __restrict__ X, int hxp, int hx, int nc,
+                           double* __restrict__ out, long long out_cstride, int out_pitch,
+                           int n_out, int nrows, Plan1D p, int NL, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 sm[];
+    const int L = p.L, ld = L + 1;
+    double2* a = sm;
+    double2* b = sm + NL * ld;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const long long line0 = (long long)blockIdx.x * NL;
+    const int rows_here = NL / nc;
+    const long long row0 = line0 / nc;
+    for (int u = tid; u < rows_here * hx * nc; u += nthr) {
+        const int rl = u / (hx * nc), q = u - rl * (hx * nc);
+        const int kx = q / nc, c = q - kx * nc;
+        const long long row = row0 + rl;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < nrows) v = X[(row * hxp + kx) * nc + c];
+        double2* s = a + (rl * nc + c) * ld;
+        s[kx] = v;
+        if (kx > 0 && L - kx >= hx) s[L - kx] = make_double2(v.x, -v.y);
+    }
+    __syncthreads();
+    double2* r = fft_lines<1>(a, b, NL, p, tid, nthr);
+    for (int u = tid; u < NL * n_out; u += nthr) {
+        const int l = u / n_out, e = u - l * n_out;
+        const long long gl = line0 + l;
+        const long long row = gl / nc;
+        const int c = (int)(gl - row * nc);
+        if (row >= nrows) continue;
+        out[c * out_cstride + row * out_pitch + e] = r[l * ld + e].x;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static const int kThreads = 256;
+static const size_t kSmemBudget = 100 * 1024;
+static const size_t kSmemMax = 200 * 1024;
+
+static int lines_per_block(int L, int multiple, size_t budget = kSmemBudget) {
+    size_t per = 2 * (size_t)(L + 1) * sizeof(double2);
+    int nl = (int)std::max<size_t>(1, budget / per);
+    nl = std::min(nl, 64);
+    nl = std::max(multiple, (nl / multiple) * multiple);
+    return nl;
+}
+
+static int set_smem_attrs() {
+    static bool done = false;
+    if (done) return MXB_OK;
+    MXB_CUDA(cudaFuncSetAttribute(k_rows_r2c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    MXB_CUDA(cudaFuncSetAttribute(k_lines<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    MXB_CUDA(cudaFuncSetAttribute(k_lines<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    MXB_CUDA(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    MXB_CUDA(cudaFuncSetAttribute(k_rows_c2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    done = true;
+    return MXB_OK;
+}
+
+static size_t smem_for(int L, int NL) { return 2 * (size_t)NL * (L + 1) * sizeof(double2); }
+
+int launch_rows_r2c(const Plan1D& p, const double* in, long long in_cstride, int in_pitch,
+                    int n_in, double2* out, int hxp, int hx, int nc, long long nrows,
+                    cudaStream_t st, const int* halt) {
+    int NL = lines_per_block(p.L, nc);
+    size_t sm = smem_for(p.L, NL);
+    if (sm > kSmemMax) { set_error("x transform length too large for the generic path"); return MXB_EINVAL; }
+    long long nlines = nrows * nc;
+    unsigned nb = (unsigned)((nlines + NL - 1) / NL);
+    k_rows_r2c<<<nb, kThreads, sm, st>>>(in, in_cstride, in_pitch, n_in, out, hxp, hx, nc,
+                                         (int)nrows, p, NL, halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int launch_lines(int dir, const Plan1D& p, const double2* in, double2* out, int n_in, int n_out,
+                 long long ES_in, long long ES_out, int Q, long long nlines, long long OS_in,
+                 long long OS_out, cudaStream_t st, const int* halt) {
+    int NL = lines_per_block(p.L, 8);
+    if (smem_for(p.L, NL) > kSmemMax) NL = lines_per_block(p.L, 1, kSmemMax);
+    size_t sm = smem_for(p.L, NL);
+    if (sm > kSmemMax) { set_error("line transform length too large for the generic path"); return MXB_EINVAL; }
+    unsigned nb = (unsigned)((nlines + NL - 1) / NL);
+    if (dir < 0)
+        k_lines<-1><<<nb, kThreads, sm, st>>>(in, out, p, n_in, n_out, ES_in, ES_out, Q, nlines,
+                                              OS_in, OS_out, NL, halt);
+    else
+        k_lines<1><<<nb, kThreads, sm, st>>>(in, out, p, n_in, n_out, ES_in, ES_out, Q, nlines,
+                                             OS_in, OS_out, NL, halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int launch_fused(const Plan1D& p, double2* X, const double2* K, int n, long long ES, int hx,
+                 int hxp, int G, long long GS, double scale, cudaStream_t st, const int* halt) {
+    int NK = std::max(1, lines_per_block(p.L, 3) / 3);
+    NK = std::min(NK, 8);
+    size_t sm = smem_for(p.L, 3 * NK);
+    if (sm > kSmemMax) { set_error("fused transform length too large for the generic path"); return MXB_EINVAL; }
+    dim3 grid((hx + NK - 1) / NK, G);
+    k_fused<<<grid, kThreads, sm, st>>>(X, K, p, n, ES, hx, hxp, G, GS, NK, scale, halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int launch_rows_c2r(const Plan1D& p, const double2* X, int hxp, int hx, int nc, double* out,
+                    long long out_cstride, int out_pitch, int n_out, long long nrows,
+                    cudaStream_t st, const int* halt) {
+    int NL = lines_per_block(p.L, nc);
+    size_t sm = smem_for(p.L, NL);
+    if (sm > kSmemMax) { set_error("x transform length too large for the generic path"); return MXB_EINVAL; }
+    long long nlines = nrows * nc;
+    unsigned nb = (unsigned)((nlines + NL - 1) / NL);
+    k_rows_c2r<<<nb, kThreads, sm, st>>>(X, hxp, hx, nc, out, out_cstride, out_pitch, n_out,
+                                         (int)nrows, p, NL, halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int DemagPlan::init(const mxb_grid& gr, int device) {
+    dev = device;
+    g.nx = (int)gr.nx; g.ny = (int)gr.ny; g.nz = (int)gr.nz;
+    g.N = (long long)gr.nx * gr.ny * gr.nz;
+    g.dx = gr.dx; g.dy = gr.dy; g.dz = gr.dz;
+    px = g.nx > 1 ? 2 * g.nx : 1;
+    py = g.ny > 1 ? 2 * g.ny : 1;
+    pz = g.nz > 1 ? 2 * g.nz : 1;
+    hx = px / 2 + 1;
+    hxp = (hx + 7) / 8 * 8;
+    scale = 1.0 / ((double)px * (double)py * (double)pz);
+    MXB_CUDA(cudaSetDevice(dev));
+    int rc = set_smem_attrs();
+    if (rc) return rc;
+    if ((rc = make_plan(px, dev, &plx, &tw[0]))) return rc;
+    if ((rc = make_plan(py, dev, &ply, &tw[1]))) return rc;
+    if ((rc = make_plan(pz, dev, &plz, &tw[2]))) return rc;
+    size_t x1 = (size_t)g.nz * g.ny * hxp * 3;
+    size_t x2 = (size_t)g.nz * py * hxp * 3;
+    MXB_CUDA(cudaMalloc(&X1, x1 * sizeof(double2)));
+    if (pz > 1 && py > 1) MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
+    else X2 = X1;
+    MXB_CUDA(cudaMalloc(&K, (size_t)pz * py * hxp * 6 * sizeof(double2)));
+    bytes = (x1 + (X2 != X1 ? x2 : 0) + (size_t)pz * py * hxp * 6) * sizeof(double2);
+    return MXB_OK;
+}
+
+void DemagPlan::release() {
+    cudaSetDevice(dev);
+    for (auto& t : tw) if (t) cudaFree(t);
+    if (X2 && X2 != X1) cudaFree(X2);
+    if (X1) cudaFree(X1);
+    if (K) cudaFree(K);
+    X1 = X2 = K = nullptr;
+}
+
+// 6 forward transforms of a packed (6,pz,py,px) device tensor into K.
+int DemagPlan::spectra_from_packed_dev(const double* P, cudaStream_t st) {
+    const long long plane = (long long)pz * py;
+    int rc = launch_rows_r2c(plx, P, plane * px, px, px, K, hxp, hx, 6, plane, st, nullptr);
+    if (rc) return rc;
+    if (py > 1) {
+        // y lines: element stride hxp*6, Q = hxp*6 per z-plane
+        rc = launch_lines(-1, ply, K, K, py, py, (long long)hxp * 6, (long long)hxp * 6, hxp * 6,
+                          (long long)pz * hxp * 6, (long long)py * hxp * 6, (long long)py * hxp * 6,
+                          st, nullptr);
+        if (rc) return rc;
+    }
+    if (pz > 1) {
+        long long Q = (long long)py * hxp * 6;
+        rc = launch_lines(-1, plz, K, K, pz, pz, Q, Q, (int)Q, Q, 0, 0, st, nullptr);
+        if (rc) return rc;
+    }
+    has_kernel = true;
+    return MXB_OK;
+}
+
+int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt) {
+    if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
+    const long long N = g.N;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    int rc;
+    // P1
+    rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, (long long)nz * ny, st, halt);
+    if (rc) return rc;
+    const long long row = (long long)hxp * 3;   // complex elements per (z,y) row
+    if (pz > 1) {
+        if (py > 1) {
+            // P2: y forward, per z-plane: ny rows in -> py rows out
+            rc = launch_lines(-1, ply, X1, X2, ny, py, row, row, (int)row, (long long)nz * row,
+                              (long long)ny * row, (long long)py * row, st, halt);
+            if (rc) return rc;
+        }
+        // P3 along z: line base = ky*row + kx*3 + c, element stride py*row
+        rc = launch_fused(plz, X2, K, nz, (long long)py * row, hx, hxp, py, row, scale, st, halt);
+        if (rc) return rc;
+        if (py > 1) {
+            rc = launch_lines(1, ply, X2, X1, py, ny, row, row, (int)row, (long long)nz * row,
+                              (long long)py * row, (long long)ny * row, st, halt);
+            if (rc) return rc;
+        }
+    } else if (py > 1) {
+        rc = launch_fused(ply, X1, K, ny, row, hx, hxp, 1, 0, scale, st, halt);
+        if (rc) return rc;
+    } else {
+        rc = launch_fused(plz, X1, K, 1, row, hx, hxp, 1, 0, scale, st, halt);
+        if (rc) return rc;
+    }
+    // P5
+    return launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, (long long)nz * ny, st, halt);
+}
+
+}  // namespace mxb

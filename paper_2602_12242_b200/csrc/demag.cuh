@@ -1,0 +1,40 @@
+#pragma once
+
+#include "common.cuh"
+#include "fft_generic.cuh"
+
+namespace mxb {
+
+struct DemagPlan {
+    int dev = 0;
+    Grid g{};
+    int px = 1, py = 1, pz = 1, hx = 1, hxp = 8;
+    double scale = 1.0;
+    Plan1D plx{}, ply{}, plz{};
+    double2* tw[3] = {nullptr, nullptr, nullptr};
+    double2* X1 = nullptr;   // [nz][ny][hxp][3]
+    double2* X2 = nullptr;   // [nz][py][hxp][3]
+    double2* K = nullptr;    // [pz][py][hxp][6] spectra (unscaled)
+    bool has_kernel = false;
+    size_t bytes = 0;
+
+    int init(const mxb_grid& g, int device);
+    void release();
+    int spectra_from_packed_dev(const double* P, cudaStream_t st);
+    int field_dev(const double* m, double* h, cudaStream_t st, const int* halt);
+};
+
+int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);
+int launch_rows_r2c(const Plan1D& p, const double* in, long long in_cstride, int in_pitch,
+                    int n_in, double2* out, int hxp, int hx, int nc, long long nrows,
+                    cudaStream_t st, const int* halt);
+int launch_lines(int dir, const Plan1D& p, const double2* in, double2* out, int n_in, int n_out,
+                 long long ES_in, long long ES_out, int Q, long long nlines, long long OS_in,
+                 long long OS_out, cudaStream_t st, const int* halt);
+
+// GPU Newell tensor builder (newell.cu)
+int newell_packed_component(const Grid& g, int comp, int symmetric, double* packed_c,
+                            double* lattice_scratch, cudaStream_t st);
+int newell_elements(const Grid& g, double* out6, double* lattice_scratch, cudaStream_t st);
+
+}  // namespace mxb

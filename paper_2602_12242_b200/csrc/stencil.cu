@@ -1,0 +1,722 @@
+// Fused local effective field + LLG torque + RK4/Euler stage update.
+//
+// One thread per cell.  Per cell it evaluates, in the reference accumulation
+// order (llg.py:112-125,170-175):
+//   exchange   flux form with harmonic face A and _StencilPlan ghosts   (fields.py:112-127)
+//   anisotropy (2Ku/mu0Ms^2)(M.eK)eK                                    (fields.py:161-163)
+//   cubic      [unpinned extension]
+//   dmi        interfacial, central differences with DMI-tilt ghosts     (fields.py:142-151)
+//   bulk dmi   [unpinned extension]
+//   demag      precomputed H_d of this stage state (demag.cu)
+//   bias       uniform vector at the stage time and/or a spatial field   (llg.py:162-164)
+// then the torque (llg.py:64-74) and the integrator stage (integrators.py:43-64),
+// with the renormalisation hook (grid.py:178-200), the pre-renormalisation
+// blow-up drift and <m> (llg.py:347-362) reduced deterministically.
+//
+// EXACT=true follows numpy's per-operation rounding (no FMA, true divisions),
+// which makes the local terms bit-identical to the reference; EXACT=false
+// lets nvcc contract and replaces constant divisions by reciprocal products.
+#include <float.h>
+#include <limits.h>
+
+#include <algorithm>
+
+#include "stencil.cuh"
+
+namespace mxb {
+
+static const int kBlock = 256;
+static const int kMaxBlocks = 148 * 16;
+
+int stage_blocks(long long N) {
+    long long nb = (N + kBlock - 1) / kBlock;
+    return (int)std::min<long long>(std::max<long long>(nb, 1), kMaxBlocks);
+}
+
+Derived derive(const MatDev& m, const Grid& g) {
+    // evaluated with plain IEEE double ops (compiled with -ffp-contract=off)
+    Derived d{};
+    const double mu0 = MXB_MU0;
+    const bool mag = m.Ms > 0.0;
+    d.pref = mag ? 2.0 / (mu0 * (m.Ms * m.Ms)) : 0.0;
+    d.pref_dmi = d.pref * m.D;
+    d.pref_an = d.pref * m.Ku;
+    d.slope_p = m.A > 0.0 ? -m.D / (2.0 * m.A) : 0.0;
+    const double tot = m.A + m.A;
+    d.face = tot > 0.0 ? 2.0 * m.A * m.A / tot : 0.0;
+    d.gl = mu0 * (m.gamma / (1.0 + m.alpha * m.alpha));
+    d.coef = mag ? d.gl * m.alpha / m.Ms : 0.0;
+    d.ms2 = m.Ms * m.Ms;
+    d.inv_ms = mag ? 1.0 / m.Ms : 0.0;
+    d.pref_cub = mag ? -2.0 * m.Kc1 / (mu0 * m.Ms) : 0.0;
+    d.pref_bdmi = -d.pref * m.Db;
+    d.slope_b = m.A > 0.0 ? m.Db / (2.0 * m.A) : 0.0;
+    (void)g;
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+// per-cell material
+// ---------------------------------------------------------------------------
+struct CellMat {
+    double Ms, A, Ku, D, alpha, ek0, ek1, ek2, Kc1, Db;
+    bool mag;
+    double pref, pref_dmi, pref_an, slope_p, gl, coef, ms2;
+};
+
+template <bool E, bool U>
+__device__ __forceinline__ CellMat cell_mat(const StageArgs& a, long long idx) {
+    CellMat c;
+    const MatDev& m = a.mat;
+    const long long N = a.g.N;
+    if (U) {
+        c.Ms = m.Ms; c.A = m.A; c.Ku = m.Ku; c.D = m.D; c.alpha = m.alpha;
+        c.ek0 = m.ek[0]; c.ek1 = m.ek[1]; c.ek2 = m.ek[2];
+        c.Kc1 = m.Kc1; c.Db = m.Db;
+        c.mag = m.Ms > 0.0;
+        c.pref = a.dv.pref; c.pref_dmi = a.dv.pref_dmi; c.pref_an = a.dv.pref_an;
+        c.slope_p = a.dv.slope_p; c.gl = a.dv.gl; c.coef = a.dv.coef; c.ms2 = a.dv.ms2;
+        return c;
+    }
+    c.Ms = m.Ms_c ? m.Ms_c[idx] : m.Ms;
+    c.A = m.A_c ? m.A_c[idx] : m.A;
+    c.Ku = m.Ku_c ? m.Ku_c[idx] : m.Ku;
+    c.D = m.D_c ? m.D_c[idx] : m.D;
+    c.alpha = m.alpha_c ? m.alpha_c[idx] : m.alpha;
+    if (m.ek_c) { c.ek0 = m.ek_c[idx]; c.ek1 = m.ek_c[N + idx]; c.ek2 = m.ek_c[2 * N + idx]; }
+    else { c.ek0 = m.ek[0]; c.ek1 = m.ek[1]; c.ek2 = m.ek[2]; }
+    c.Kc1 = m.Kc1; c.Db = m.Db;
+    c.mag = c.Ms > 0.0;
+    c.ms2 = mul<E>(c.Ms, c.Ms);
+    c.pref = c.mag ? div_rn(2.0, mul<E>(MXB_MU0, c.ms2)) : 0.0;
+    c.pref_dmi = mul<E>(c.pref, c.D);
+    c.pref_an = mul<E>(c.pref, c.Ku);
+    c.slope_p = c.A > 0.0 ? div_rn(-c.D, mul<E>(2.0, c.A)) : 0.0;
+    c.gl = mul<E>(MXB_MU0, div_rn(m.gamma, add<E>(1.0, mul<E>(c.alpha, c.alpha))));
+    c.coef = c.mag ? div_rn(mul<E>(c.gl, c.alpha), c.Ms) : 0.0;
+    return c;
+}
+
+__device__ __forceinline__ double ld(const double* p, long long i) { return __ldg(p + i); }
+
+// Neighbour of cell idx along `axis` (0 x, 1 y, 2 z) in direction `step`,
+// exactly as _StencilPlan.neighbor + a_face (fields.py:59-92).
+template <bool E, bool U>
+__device__ __forceinline__ void neighbour(const StageArgs& a, const double* f, long long idx,
+                                          int coord, int n, long long stride, int step, int axis,
+                                          const double m[3], const CellMat& cm, double nb[3],
+                                          double& face) {
+    const long long N = a.g.N;
+    const bool periodic = a.ghost == MXB_GHOST_PERIODIC;
+    const int c2 = coord + step;
+    const bool inr = c2 >= 0 && c2 < n;
+    long long nidx;
+    if (periodic) {
+        const int w = inr ? c2 : (c2 < 0 ? c2 + n : c2 - n);
+        nidx = idx + (long long)(w - coord) * stride;
+    } else {
+        nidx = inr ? idx + step * stride : idx;
+    }
+    bool valid;
+    double Anb;
+    if (U) {
+        valid = (periodic || inr) && cm.mag;
+        Anb = cm.A;
+    } else {
+        const double msn = a.mat.Ms_c ? ld(a.mat.Ms_c, nidx) : a.mat.Ms;
+        valid = (periodic || inr) && msn > 0.0;
+        Anb = a.mat.A_c ? ld(a.mat.A_c, nidx) : a.mat.A;
+    }
+    double harm;
+    if (U) {
+        harm = a.dv.face;
+    } else {
+        const double tot = add<E>(cm.A, Anb);
+        harm = tot > 0.0 ? div_rn(mul<E>(mul<E>(2.0, cm.A), Anb), tot) : 0.0;
+    }
+    face = valid ? harm : cm.A;
+    if (periodic || valid) {
+        nb[0] = ld(f, nidx);
+        nb[1] = ld(f, N + nidx);
+        nb[2] = ld(f, 2 * N + nidx);
+    } else if (a.ghost == MXB_GHOST_NEUMANN) {
+        nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];
+    } else {
+        // DMI tilt: M + (step*d) * slope (grid.py:217-235)
+        const double d = axis == 0 ? a.g.dx : (axis == 1 ? a.g.dy : a.g.dz);
+        const double sd = step > 0 ? d : -d;
+        const double p = cm.slope_p;
+        if (axis == 0) {
+            nb[0] = add<E>(m[0], mul<E>(sd, mul<E>(p, m[2])));
+            nb[1] = add<E>(m[1], mul<E>(sd, 0.0));
+            nb[2] = add<E>(m[2], mul<E>(sd, mul<E>(-p, m[0])));
+        } else if (axis == 1) {
+            nb[0] = add<E>(m[0], mul<E>(sd, 0.0));
+            nb[1] = add<E>(m[1], mul<E>(sd, mul<E>(p, m[2])));
+            nb[2] = add<E>(m[2], mul<E>(sd, mul<E>(-p, m[1])));
+        } else {
+            nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];
+        }
+    }
+}
+
+// bulk-DMI neighbour: raw neighbour if in range and magnetic, else the
+// natural-boundary ghost M + step*d*(Db/2A)(e_k x M)   [unpinned extension]
+template <bool U>
+__device__ __forceinline__ void bulk_neighbour(const StageArgs& a, const double* f, long long idx,
+                                               int coord, int n, long long stride, int step,
+                                               int axis, const double m[3], const CellMat& cm,
+                                               double nb[3]) {
+    const long long N = a.g.N;
+    const int c2 = coord + step;
+    bool valid = c2 >= 0 && c2 < n;
+    const long long nidx = valid ? idx + step * stride : idx;
+    if (valid && !U && a.mat.Ms_c) valid = ld(a.mat.Ms_c, nidx) > 0.0;
+    if (valid) {
+        nb[0] = ld(f, nidx); nb[1] = ld(f, N + nidx); nb[2] = ld(f, 2 * N + nidx);
+        return;
+    }
+    const double d = axis == 0 ? a.g.dx : (axis == 1 ? a.g.dy : a.g.dz);
+    const double sd = step > 0 ? d : -d;
+    const double pr = U ? a.dv.slope_b : (cm.A > 0.0 ? cm.Db / (2.0 * cm.A) : 0.0);
+    double cr[3];
+    if (axis == 0) { cr[0] = 0.0; cr[1] = -m[2]; cr[2] = m[1]; }
+    else if (axis == 1) { cr[0] = m[2]; cr[1] = 0.0; cr[2] = -m[0]; }
+    else { cr[0] = -m[1]; cr[1] = m[0]; cr[2] = 0.0; }
+    for (int q = 0; q < 3; ++q) nb[q] = m[q] + sd * (pr * cr[q]);
+}
+
+// H_eff of one cell in the reference accumulation order.
+template <bool E, bool U>
+__device__ __forceinline__ void heff_cell(const StageArgs& a, const double* f, long long idx, int i,
+                                          int j, int k, const double m[3], const CellMat& cm,
+                                          uint32_t terms, double h[3]) {
+    const Grid& g = a.g;
+    h[0] = 0.0; h[1] = 0.0; h[2] = 0.0;
+    const bool ex = terms & MXB_TERM_EXCHANGE;
+    const bool dmi = terms & MXB_TERM_DMI;
+    double xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
+    double fxp = 0, fxm = 0, fyp = 0, fym = 0, fzp = 0, fzm = 0;
+    const bool need_x = (ex && g.nx > 1) || dmi;
+    const bool need_y = (ex && g.ny > 1) || dmi;
+    const bool need_z = ex && g.nz > 1;
+    const long long sy = g.nx, sz = (long long)g.nx * g.ny;
+    if (need_x) {
+        neighbour<E, U>(a, f, idx, i, g.nx, 1, +1, 0, m, cm, xp, fxp);
+        neighbour<E, U>(a, f, idx, i, g.nx, 1, -1, 0, m, cm, xm, fxm);
+    }
+    if (need_y) {
+        neighbour<E, U>(a, f, idx, j, g.ny, sy, +1, 1, m, cm, yp, fyp);
+        neighbour<E, U>(a, f, idx, j, g.ny, sy, -1, 1, m, cm, ym, fym);
+    }
+    if (need_z) {
+        neighbour<E, U>(a, f, idx, k, g.nz, sz, +1, 2, m, cm, zp, fzp);
+        neighbour<E, U>(a, f, idx, k, g.nz, sz, -1, 2, m, cm, zm, fzm);
+    }
+    if (ex) {
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (g.nx > 1) {
+            const double dd = mul<E>(g.dx, g.dx);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double t = sub<E>(mul<E>(fxp, sub<E>(xp[q], m[q])), mul<E>(fxm, sub<E>(m[q], xm[q])));
+                acc[q] = add<E>(acc[q], E ? div_rn(t, dd) : t * (1.0 / dd));
+            }
+        }
+        if (g.ny > 1) {
+            const double dd = mul<E>(g.dy, g.dy);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double t = sub<E>(mul<E>(fyp, sub<E>(yp[q], m[q])), mul<E>(fym, sub<E>(m[q], ym[q])));
+                acc[q] = add<E>(acc[q], E ? div_rn(t, dd) : t * (1.0 / dd));
+            }
+        }
+        if (g.nz > 1) {
+            const double dd = mul<E>(g.dz, g.dz);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double t = sub<E>(mul<E>(fzp, sub<E>(zp[q], m[q])), mul<E>(fzm, sub<E>(m[q], zm[q])));
+                acc[q] = add<E>(acc[q], E ? div_rn(t, dd) : t * (1.0 / dd));
+            }
+        }
+        if (cm.mag) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) h[q] = add<E>(h[q], mul<E>(cm.pref, acc[q]));
+        }
+    }
+    if (terms & MXB_TERM_ANISOTROPY) {
+        const double proj = add<E>(add<E>(mul<E>(m[0], cm.ek0), mul<E>(m[1], cm.ek1)), mul<E>(m[2], cm.ek2));
+        const double t = mul<E>(cm.pref_an, proj);
+        h[0] = add<E>(h[0], mul<E>(t, cm.ek0));
+        h[1] = add<E>(h[1], mul<E>(t, cm.ek1));
+        h[2] = add<E>(h[2], mul<E>(t, cm.ek2));
+    }
+    if ((terms & MXB_TERM_CUBIC) && cm.mag) {
+        const MatDev& mt = a.mat;
+        const double inv = 1.0 / cm.Ms;
+        const double mn0 = m[0] * inv, mn1 = m[1] * inv, mn2 = m[2] * inv;
+        const double a1 = mt.c1[0] * mn0 + mt.c1[1] * mn1 + mt.c1[2] * mn2;
+        const double a2 = mt.c2[0] * mn0 + mt.c2[1] * mn1 + mt.c2[2] * mn2;
+        const double a3 = mt.c3[0] * mn0 + mt.c3[1] * mn1 + mt.c3[2] * mn2;
+        const double p = U ? a.dv.pref_cub : -2.0 * cm.Kc1 / (MXB_MU0 * cm.Ms);
+        const double w1 = p * a1 * (a2 * a2 + a3 * a3);
+        const double w2 = p * a2 * (a3 * a3 + a1 * a1);
+        const double w3 = p * a3 * (a1 * a1 + a2 * a2);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) h[q] += w1 * mt.c1[q] + w2 * mt.c2[q] + w3 * mt.c3[q];
+    }
+    if (dmi) {
+        const double i2x = 2 * g.dx, i2y = 2 * g.dy;
+        const double gx0 = E ? div_rn(sub<E>(xp[0], xm[0]), i2x) : (xp[0] - xm[0]) * (1.0 / i2x);
+        const double gx2 = E ? div_rn(sub<E>(xp[2], xm[2]), i2x) : (xp[2] - xm[2]) * (1.0 / i2x);
+        const double gy1 = E ? div_rn(sub<E>(yp[1], ym[1]), i2y) : (yp[1] - ym[1]) * (1.0 / i2y);
+        const double gy2 = E ? div_rn(sub<E>(yp[2], ym[2]), i2y) : (yp[2] - ym[2]) * (1.0 / i2y);
+        if (cm.mag) {
+            h[0] = add<E>(h[0], mul<E>(cm.pref_dmi, gx2));
+            h[1] = add<E>(h[1], mul<E>(cm.pref_dmi, gy2));
+            h[2] = add<E>(h[2], mul<E>(-cm.pref_dmi, add<E>(gx0, gy1)));
+        }
+    }
+    if ((terms & MXB_TERM_BULK_DMI) && cm.mag) {
+        double bp[3], bm[3], gr[3][3];
+        const int coords[3] = {i, j, k};
+        const int ns[3] = {g.nx, g.ny, g.nz};
+        const long long strides[3] = {1, sy, sz};
+        const double ds[3] = {g.dx, g.dy, g.dz};
+        for (int ax = 0; ax < 3; ++ax) {
+            bulk_neighbour<U>(a, f, idx, coords[ax], ns[ax], strides[ax], +1, ax, m, cm, bp);
+            bulk_neighbour<U>(a, f, idx, coords[ax], ns[ax], strides[ax], -1, ax, m, cm, bm);
+            for (int q = 0; q < 3; ++q) gr[ax][q] = (bp[q] - bm[q]) / (2 * ds[ax]);
+        }
+        const double cx = gr[1][2] - gr[2][1];
+        const double cy = gr[2][0] - gr[0][2];
+        const double cz = gr[0][1] - gr[1][0];
+        const double p = U ? a.dv.pref_bdmi : -(cm.pref * cm.Db);
+        h[0] += p * cx; h[1] += p * cy; h[2] += p * cz;
+    }
+    if (terms & MXB_TERM_DEMAG) {
+        const long long N = g.N;
+        h[0] = add<E>(h[0], ld(a.hd, idx));
+        h[1] = add<E>(h[1], ld(a.hd, N + idx));
+        h[2] = add<E>(h[2], ld(a.hd, 2 * N + idx));
+    }
+    if (terms & MXB_TERM_BIAS) {
+        double b0 = a.bias[0], b1 = a.bias[1], b2 = a.bias[2];
+        if (a.bias_field) {
+            const long long N = g.N;
+            b0 = ld(a.bias_field, idx); b1 = ld(a.bias_field, N + idx); b2 = ld(a.bias_field, 2 * N + idx);
+        }
+        h[0] = add<E>(h[0], b0);
+        h[1] = add<E>(h[1], b1);
+        h[2] = add<E>(h[2], b2);
+    }
+}
+
+template <bool E>
+__device__ __forceinline__ void torque(const double m[3], const double h[3], const CellMat& cm,
+                                       int prec, int damp, double k[3]) {
+    const double x0 = sub<E>(mul<E>(m[1], h[2]), mul<E>(m[2], h[1]));
+    const double x1 = sub<E>(mul<E>(m[2], h[0]), mul<E>(m[0], h[2]));
+    const double x2 = sub<E>(mul<E>(m[0], h[1]), mul<E>(m[1], h[0]));
+    k[0] = 0.0; k[1] = 0.0; k[2] = 0.0;
+    if (prec) {
+        k[0] = add<E>(k[0], mul<E>(cm.gl, x0));
+        k[1] = add<E>(k[1], mul<E>(cm.gl, x1));
+        k[2] = add<E>(k[2], mul<E>(cm.gl, x2));
+    }
+    if (damp) {
+        const double y0 = sub<E>(mul<E>(m[1], x2), mul<E>(m[2], x1));
+        const double y1 = sub<E>(mul<E>(m[2], x0), mul<E>(m[0], x2));
+        const double y2 = sub<E>(mul<E>(m[0], x1), mul<E>(m[1], x0));
+        k[0] = add<E>(k[0], mul<E>(cm.coef, y0));
+        k[1] = add<E>(k[1], mul<E>(cm.coef, y1));
+        k[2] = add<E>(k[2], mul<E>(cm.coef, y2));
+    }
+}
+
+// renormalize one cell (grid.py:184-200); returns false on a dead magnetic cell
+template <bool E>
+__device__ __forceinline__ bool renorm_cell(double v[3], const CellMat& cm) {
+    const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
+    if (cm.mag && n2 == 0.0) return false;
+    const bool stale = cm.mag && fabs(sub<E>(n2, cm.ms2)) > mul<E>(1e-15, cm.ms2);
+    double s = 1.0;
+    if (stale) s = E ? div_rn(cm.Ms, sqrt(n2)) : cm.Ms * rsqrt(n2);
+    if (!cm.mag) s = 0.0;
+    v[0] = mul<E>(v[0], s); v[1] = mul<E>(v[1], s); v[2] = mul<E>(v[2], s);
+    return true;
+}
+
+__device__ __forceinline__ void flag_dead(Ctl* ctl, long long idx) {
+    atomicMin((long long*)&ctl->dead_flat, idx);
+    atomicCAS(&ctl->halt, 0, (int)MXB_EDEAD);
+}
+
+// ---------------------------------------------------------------------------
+// block reductions (deterministic for a fixed launch shape)
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_reduce(double v[NV], const bool is_max[NV]) {
+    __shared__ double sh[32][NV];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_down_sync(0xffffffffu, v[q], o);
+            v[q] = is_max[q] ? fmax(v[q], w) : v[q] + w;
+        }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) sh[wid][q] = v[q];
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            v[q] = lane < nw ? sh[lane][q] : (is_max[q] ? -DBL_MAX : 0.0);
+            for (int o = 16; o > 0; o >>= 1) {
+                const double w = __shfl_down_sync(0xffffffffu, v[q], o);
+                v[q] = is_max[q] ? fmax(v[q], w) : v[q] + w;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+__device__ bool last_block_done(Ctl* ctl) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+        const unsigned prev = atomicInc(&ctl->arrive, total - 1);
+        last = prev == total - 1;
+    }
+    __syncthreads();
+    return last;
+}
+
+// final reduction of NV partial slots over all blocks, by the last block
+template <int NV>
+__device__ void reduce_partials(const double* partials, int nblk, const bool is_max[NV],
+                                double out[NV]) {
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = is_max[q] ? -DBL_MAX : 0.0;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+        volatile const double* p = partials + (long long)b * kReduceSlots;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = is_max[q] ? fmax(v[q], p[q]) : v[q] + p[q];
+    }
+    block_reduce<NV>(v, is_max);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) out[q] = v[q];
+}
+
+// ---------------------------------------------------------------------------
+// the fused stage kernel
+// ---------------------------------------------------------------------------
+template <int MODE, bool E, bool U>
+__global__ void __launch_bounds__(256) k_stage(StageArgs a) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    const Grid& g = a.g;
+    const long long N = g.N;
+    constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % g.nx);
+        const long long r = idx / g.nx;
+        const int j = (int)(r % g.ny), k = (int)(r / g.ny);
+        const CellMat cm = cell_mat<E, U>(a, idx);
+        const double m[3] = {ld(a.ys, idx), ld(a.ys, N + idx), ld(a.ys, 2 * N + idx)};
+        double h[3];
+        heff_cell<E, U>(a, a.ys, idx, i, j, k, m, cm, a.terms, h);
+        if (MODE == M_HEFF) {
+            a.out[idx] = h[0]; a.out[N + idx] = h[1]; a.out[2 * N + idx] = h[2];
+            continue;
+        }
+        double kk[3];
+        torque<E>(m, h, cm, a.prec, a.damp, kk);
+        if (MODE == M_RHS) {
+            a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
+            continue;
+        }
+        const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
+        double v[3];
+        if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) v[q] = add<E>(y[q], mul<E>(a.c, kk[q]));
+            if (MODE == M_RK1) {
+                a.k1_out[idx] = kk[0]; a.k1_out[N + idx] = kk[1]; a.k1_out[2 * N + idx] = kk[2];
+            } else if (MODE == M_RK2) {
+                a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
+            } else if (MODE == M_RK3) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
+            }
+        } else {  // M_RK4
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
+                v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
+            }
+        }
+        if (kFinal) {
+            if (cm.mag) {
+                const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
+                double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
+                if (!(d == d) || isinf(d)) d = DBL_MAX;  // non-finite drift (llg.py:351)
+                red[3] = fmax(red[3], d);
+            }
+            // a dead cell here always has drift 1 > 0.1, so the blow-up wins
+            // (llg.py:348-355); only record it, never halt mid-kernel
+            if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
+            if (cm.mag) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    red[q] = red[q] + (E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms));
+            }
+        } else if (a.renorm) {
+            if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
+        }
+        a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
+    }
+    if (kFinal) {
+        const bool is_max[4] = {false, false, false, true};
+        block_reduce<4>(red, is_max);
+        if (threadIdx.x == 0) {
+            double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
+            p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = red[3];
+        }
+        if (last_block_done(a.ctl)) {
+            double tot[4];
+            reduce_partials<4>(a.partials, gridDim.x, is_max, tot);
+            if (threadIdx.x == 0) {
+                Ctl* c = a.ctl;
+                const double drift = tot[3] < 0.0 ? 0.0 : tot[3];
+                if (drift == DBL_MAX || drift > 0.10) {
+                    c->drift = drift;
+                    c->halt = MXB_EBLOWUP;
+                } else if (c->halt == 0) {
+                    const double inv = (double)c->n_magnetic;
+                    double res = 0.0;
+                    for (int q = 0; q < 3; ++q) {
+                        const double mq = tot[q] / inv;
+                        res = fmax(res, fabs(mq - c->prev_mean[q]));
+                        c->mean[q] = mq;
+                        c->prev_mean[q] = mq;
+                    }
+                    c->residual = res;
+                    c->drift = drift;
+                    c->steps_done += 1;
+                    if (c->eq_tol >= 0.0 && res < c->eq_tol) c->halt = MXB_EQUILIBRATED;
+                }
+                __threadfence();
+            }
+        }
+    }
+}
+
+template <int MODE, bool E>
+static void launch_mode_u(const StageArgs& a, cudaStream_t st, int nb) {
+    if (a.mat.uniform) k_stage<MODE, E, true><<<nb, kBlock, 0, st>>>(a);
+    else k_stage<MODE, E, false><<<nb, kBlock, 0, st>>>(a);
+}
+
+template <int MODE>
+static void launch_mode(bool exact, const StageArgs& a, cudaStream_t st, int nb) {
+    if (exact) launch_mode_u<MODE, true>(a, st, nb);
+    else launch_mode_u<MODE, false>(a, st, nb);
+}
+
+int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    switch (mode) {
+        case M_HEFF: launch_mode<M_HEFF>(exact, a, st, nb); break;
+        case M_RHS: launch_mode<M_RHS>(exact, a, st, nb); break;
+        case M_RK1: launch_mode<M_RK1>(exact, a, st, nb); break;
+        case M_RK2: launch_mode<M_RK2>(exact, a, st, nb); break;
+        case M_RK3: launch_mode<M_RK3>(exact, a, st, nb); break;
+        case M_RK4: launch_mode<M_RK4>(exact, a, st, nb); break;
+        case M_EULER: launch_mode<M_EULER>(exact, a, st, nb); break;
+        default: set_error("bad stage mode"); return MXB_EINVAL;
+    }
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+// a single field term (ExchangeOperator etc.): H of only `term`
+int launch_term(uint32_t term, int ghost, bool exact, const StageArgs& a0, cudaStream_t st) {
+    StageArgs a = a0;
+    a.terms = term;
+    a.ghost = ghost;
+    return launch_stage(M_HEFF, exact, a, st);
+}
+
+// ---------------------------------------------------------------------------
+// renormalize / mean / energies
+// ---------------------------------------------------------------------------
+template <bool U>
+__global__ void k_renorm(StageArgs a, double* m) {
+    const long long N = a.g.N;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const CellMat cm = cell_mat<true, U>(a, idx);
+        double v[3] = {m[idx], m[N + idx], m[2 * N + idx]};
+        if (!renorm_cell<true>(v, cm)) {
+            atomicMin((long long*)&a.ctl->dead_flat, idx);
+            continue;
+        }
+        m[idx] = v[0]; m[N + idx] = v[1]; m[2 * N + idx] = v[2];
+    }
+}
+
+int launch_renorm(const StageArgs& a, double* m, cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    if (a.mat.uniform) k_renorm<true><<<nb, kBlock, 0, st>>>(a, m);
+    else k_renorm<false><<<nb, kBlock, 0, st>>>(a, m);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+template <bool U>
+__global__ void k_mean(StageArgs a, const double* m) {
+    const long long N = a.g.N;
+    double red[3] = {0.0, 0.0, 0.0};
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const CellMat cm = cell_mat<true, U>(a, idx);
+        if (!cm.mag) continue;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) red[q] += div_rn(m[q * N + idx], cm.Ms);
+    }
+    const bool is_max[3] = {false, false, false};
+    block_reduce<3>(red, is_max);
+    if (threadIdx.x == 0) {
+        double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
+        p[0] = red[0]; p[1] = red[1]; p[2] = red[2];
+    }
+    if (last_block_done(a.ctl)) {
+        double tot[3];
+        reduce_partials<3>(a.partials, gridDim.x, is_max, tot);
+        if (threadIdx.x == 0)
+            for (int q = 0; q < 3; ++q) a.ctl->mean[q] = tot[q] / (double)a.ctl->n_magnetic;
+    }
+}
+
+int launch_mean(const StageArgs& a, const double* m, cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    if (a.mat.uniform) k_mean<true><<<nb, kBlock, 0, st>>>(a, m);
+    else k_mean<false><<<nb, kBlock, 0, st>>>(a, m);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+// energy densities (fields.py:200-242) summed over magnetic cells
+template <bool E, bool U>
+__global__ void k_energies(StageArgs a, const double* m, const double* hd) {
+    const Grid& g = a.g;
+    const long long N = g.N;
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    const bool dmi_mode = a.ghost == MXB_GHOST_DMI;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const CellMat cm = cell_mat<E, U>(a, idx);
+        if (!cm.mag) continue;
+        const int i = (int)(idx % g.nx);
+        const long long r = idx / g.nx;
+        const int j = (int)(r % g.ny), k = (int)(r / g.ny);
+        const double mv[3] = {m[idx], m[N + idx], m[2 * N + idx]};
+        if (hd) {
+            const double dot = add<E>(add<E>(mul<E>(mv[0], hd[idx]), mul<E>(mv[1], hd[N + idx])),
+                                      mul<E>(mv[2], hd[2 * N + idx]));
+            red[0] += mul<E>(-0.5 * MXB_MU0, dot);
+        }
+        // normalised m and its neighbours (plan.neighbor on mn)
+        const double mn[3] = {div_rn(mv[0], cm.Ms), div_rn(mv[1], cm.Ms), div_rn(mv[2], cm.Ms)};
+        double g2 = 0.0;
+        const int coords[3] = {i, j, k};
+        const int ns[3] = {g.nx, g.ny, g.nz};
+        const long long strides[3] = {1, g.nx, (long long)g.nx * g.ny};
+        const double ds[3] = {g.dx, g.dy, g.dz};
+        for (int ax = 0; ax < 3; ++ax) {
+            if (ns[ax] == 1 && !dmi_mode) continue;
+            double nb[2][3];
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                const int step = sgn == 0 ? 1 : -1;
+                const bool periodic = a.ghost == MXB_GHOST_PERIODIC;
+                const int c2 = coords[ax] + step;
+                const bool inr = c2 >= 0 && c2 < ns[ax];
+                long long nidx;
+                if (periodic) {
+                    const int w = inr ? c2 : (c2 < 0 ? c2 + ns[ax] : c2 - ns[ax]);
+                    nidx = idx + (long long)(w - coords[ax]) * strides[ax];
+                } else {
+                    nidx = inr ? idx + step * strides[ax] : idx;
+                }
+                const double msn = U ? a.mat.Ms : (a.mat.Ms_c ? a.mat.Ms_c[nidx] : a.mat.Ms);
+                const bool valid = (periodic || inr) && msn > 0.0;
+                if (periodic || valid) {
+                    for (int q = 0; q < 3; ++q) nb[sgn][q] = msn > 0.0 ? div_rn(m[q * N + nidx], msn) : 0.0;
+                } else if (a.ghost == MXB_GHOST_NEUMANN || ax == 2) {
+                    for (int q = 0; q < 3; ++q) nb[sgn][q] = mn[q];
+                } else {
+                    const double sd = step > 0 ? ds[ax] : -ds[ax];
+                    const double p = cm.slope_p;
+                    if (ax == 0) {
+                        nb[sgn][0] = add<E>(mn[0], mul<E>(sd, mul<E>(p, mn[2])));
+                        nb[sgn][1] = add<E>(mn[1], mul<E>(sd, 0.0));
+                        nb[sgn][2] = add<E>(mn[2], mul<E>(sd, mul<E>(-p, mn[0])));
+                    } else {
+                        nb[sgn][0] = add<E>(mn[0], mul<E>(sd, 0.0));
+                        nb[sgn][1] = add<E>(mn[1], mul<E>(sd, mul<E>(p, mn[2])));
+                        nb[sgn][2] = add<E>(mn[2], mul<E>(sd, mul<E>(-p, mn[1])));
+                    }
+                }
+            }
+            const double d2 = 2 * ds[ax];
+            const double q0 = div_rn(sub<E>(nb[0][0], nb[1][0]), d2);
+            const double q1 = div_rn(sub<E>(nb[0][1], nb[1][1]), d2);
+            const double q2 = div_rn(sub<E>(nb[0][2], nb[1][2]), d2);
+            g2 = add<E>(g2, add<E>(add<E>(mul<E>(q0, q0), mul<E>(q1, q1)), mul<E>(q2, q2)));
+        }
+        red[1] += mul<E>(cm.A, g2);
+        const double pr = add<E>(add<E>(mul<E>(mn[0], cm.ek0), mul<E>(mn[1], cm.ek1)), mul<E>(mn[2], cm.ek2));
+        red[2] += mul<E>(cm.Ku, sub<E>(1.0, mul<E>(pr, pr)));
+        if (a.terms & MXB_TERM_BIAS) {
+            double b0 = a.bias[0], b1 = a.bias[1], b2 = a.bias[2];
+            if (a.bias_field) { b0 = a.bias_field[idx]; b1 = a.bias_field[N + idx]; b2 = a.bias_field[2 * N + idx]; }
+            const double dot = add<E>(add<E>(mul<E>(mv[0], b0), mul<E>(mv[1], b1)), mul<E>(mv[2], b2));
+            red[3] += mul<E>(-MXB_MU0, dot);
+        }
+    }
+    const bool is_max[4] = {false, false, false, false};
+    block_reduce<4>(red, is_max);
+    if (threadIdx.x == 0) {
+        double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
+        p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = red[3];
+    }
+    if (last_block_done(a.ctl)) {
+        double tot[4];
+        reduce_partials<4>(a.partials, gridDim.x, is_max, tot);
+        if (threadIdx.x == 0)
+            for (int q = 0; q < 4; ++q) a.ctl->energies[q] = tot[q] / (double)a.ctl->n_magnetic;
+    }
+}
+
+int launch_energies(bool exact, const StageArgs& a, const double* m, const double* hd,
+                    cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    if (exact) {
+        if (a.mat.uniform) k_energies<true, true><<<nb, kBlock, 0, st>>>(a, m, hd);
+        else k_energies<true, false><<<nb, kBlock, 0, st>>>(a, m, hd);
+    } else {
+        if (a.mat.uniform) k_energies<false, true><<<nb, kBlock, 0, st>>>(a, m, hd);
+        else k_energies<false, false><<<nb, kBlock, 0, st>>>(a, m, hd);
+    }
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+}  // namespace mxb
