@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""LLG cell-steps/s (fp64 RK4, full H_eff) on B200 -- BASELINE.json metric.
+
+Workload (N=1): synthetic random-m 512^3 grid (BASELINE configs[3]), 4 nm
+cells, Ms=8e5 A/m, A=1.3e-11 J/m, Ku=5e4 J/m^3 along z, interfacial D=1e-3
+J/m^2, alpha=0.1, Zeeman (1e4,0,0) A/m, FFT demag (GPU-built Newell tensor),
+DMI ghost boundaries; m from numpy default_rng(0) normals, renormalised;
+dt = 0.1 * stable_dt (bench/common.py:40-48) so no step blows up.
+
+One "step" = one full RK4 step (4 demag evaluations + 4 fused stencil/LLG/
+stage kernels).  value = cells * K / device time of K steps (CUDA events on
+the context stream, after W warm-up steps); inputs (3.2 GB per field) are
+larger than the 126 MB L2, so no explicit flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512] [--impl reference]
+
+Under torchrun (N>1) every rank runs its own replica of the workload (the
+z-slab decomposition is not wired into the bench yet); the step time is the
+max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+METRIC = "LLG cell-steps/s (fp64 RK4, full H_eff) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def setup_problem(n: int):
+    import paper_2602_12242_b200 as mx
+    from paper_2602_12242_b200.llg import _ORDER
+    g = mx.GridSpec(n, n, n, 4e-9, 4e-9, 4e-9)
+    mat = mx.MaterialMap(g, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
+    t0 = time.perf_counter()
+    kern = mx.DemagKernel.build(g, symmetric=True)
+    t_build = time.perf_counter() - t0
+    bias = np.array([1e4, 0.0, 0.0])
+    rhs = mx.PartitionedRHS(mat, exchange=True, anisotropy=True, dmi=True, demag=kern, bias=bias)
+    rng = np.random.default_rng(0)
+    m = mx.VectorField3(g, rng.standard_normal(size=(3,) + g.shape))
+    mx.renormalize(m, mat)
+    dt = 0.1 * 0.5 * 2.5e-14 * (4e-9 / 0.78125e-9) ** 2   # 0.1 * stable_dt(4 nm, permalloy)
+    return mx, g, mat, kern, rhs, m, dt, bias, t_build
+
+
+def demag_bytes(g, kern):
+    """Algorithmic HBM bytes of one demag evaluation, per pass."""
+    nx, ny, nz = g.nx, g.ny, g.nz
+    pz, py, px = kern.padded
+    hx = px // 2 + 1
+    N = nx * ny * nz
+    kbytes = (48 if kern.symmetric else 96) * hx * py * pz
+    x1 = 48 * hx * ny * nz
+    x2 = 48 * hx * py * nz
+    return [24 * N + x1, x1 + x2, 2 * x2 + kbytes, x2 + x1, x1 + 24 * N]
+
+
+def cpu_reference(n: int, steps: int, warmup: int):
+    """Oracle (numpy/scipy restatement of the reference) RK4 on a bounded
+    sample of the same workload: an n^3 grid, all host threads for the FFTs."""
+    from oracle import magnex_oracle as O
+    cores = os.cpu_count() or 1
+    mat = O.make_mat((n, n, n), (4e-9,) * 3, 8e5, A=1.3e-11, Ku=5e4, D=1e-3, alpha=0.1)
+    spectra = O.kernel_spectra(O.packed_tensor(n, n, n, 4e-9, 4e-9, 4e-9), workers=cores)
+    import scipy.fft as sfft
+    terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=spectra,
+                    bias=np.array([1e4, 0.0, 0.0]))
+    rng = np.random.default_rng(0)
+    m = O.renormalize(rng.standard_normal(size=(3, n, n, n)), mat)
+    dt = 0.1 * O.stable_dt(4e-9, 1.3e-11, 8e5)
+    with sfft.set_workers(cores):
+        if warmup:
+            m = O.run(m, mat, terms, "rk4", dt, max_steps=warmup).m
+        t0 = time.perf_counter()
+        r = O.run(m, mat, terms, "rk4", dt, max_steps=steps)
+        el = time.perf_counter() - t0
+    return n ** 3 * steps / el, el, cores
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-n", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cs, el, cores = cpu_reference(args.cpu_n, max(args.steps, 1), max(args.warmup, 0))
+        out = {"metric": METRIC, "value": cs, "unit": "cell-steps/s", "n_gpus": args.gpus,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "impl": "reference",
+               "config": {"workload": f"synthetic random-m {args.cpu_n}^3 full H_eff RK4 "
+                                      f"(bounded CPU sample of the {args.n}^3 workload)"},
+               "cpu_baseline": {"value": cs, "unit": "cell-steps/s", "cores": cores, "kind": "port",
+                                "sample": f"{args.cpu_n}^3, {args.steps} RK4 steps, oracle numpy/scipy"},
+               "e2e": {"value": cs, "unit": "cell-steps/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    import ctypes as C
+
+    import paper_2602_12242_b200 as mxb
+    from paper_2602_12242_b200 import _lib as L
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    mxb.set_device(local)
+    mx, g, mat, kern, rhs, m, dt, bias, t_build = setup_problem(args.n)
+    N = g.n_cells
+    ctx = mat._ctx()
+    L.check(ctx.call("mxb_state_set", L.dptr(m.data)))
+    from paper_2602_12242_b200.llg import _ORDER
+    ts = rhs._terms_struct(tuple(x for x in _ORDER if x in rhs.enabled_terms()))
+    bptr = L.dptr(np.ascontiguousarray(bias))
+    ms_tot, ms_st = C.c_double(), C.c_double()
+    nl = C.c_int64()
+    d = kern._d.h
+    # warm-up
+    L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, max(args.warmup, 1), bptr,
+                     C.byref(ms_tot), None, C.byref(nl)))
+    if world > 1:
+        dist.barrier()
+    with Clocks(local) as clk:
+        L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, args.steps, bptr,
+                         C.byref(ms_tot), C.byref(ms_st), C.byref(nl)))
+    t_step = ms_tot.value / args.steps
+    if world > 1:
+        import torch
+        t = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = world * N / (t_step * 1e-3)
+    # per-kernel timing for the roofline
+    ms_eval = C.c_double()
+    passes = np.zeros(5)
+    L.check(ctx.call("mxb_time_demag", d, 3, C.byref(ms_eval), L.dptr(passes)))
+    ms_cufft = C.c_double(float("nan"))
+    rc = L.load().mxb_time_demag_cufft(d, 3, C.byref(ms_cufft))
+    if rc != 0:
+        ms_cufft = C.c_double(float("nan"))
+    hbm, which = peaks()
+    pb = demag_bytes(g, kern)
+    stencil_bytes = 504 * N               # per RK4 step (4 fused stage kernels)
+    kernels = [("x_r2c", pb[0], passes[0]), ("y_fwd", pb[1], passes[1]),
+               ("z_fused_mul", pb[2], passes[2]), ("y_inv", pb[3], passes[3]),
+               ("x_c2r", pb[4], passes[4]),
+               ("stage_stencil_llg", stencil_bytes / 4, ms_st.value / args.steps / 4)]
+    share = {k: 4 * t for k, _, t in kernels}
+    dom = max(kernels, key=lambda x: x[2])
+    ach = dom[1] / (dom[2] * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom[0])
+    except Exception:
+        pass
+    step_bytes = stencil_bytes + 4 * sum(pb)
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = C.c_void_p()
+        L.check(L.load().mxb_host_alloc(m.data.nbytes, C.byref(pinned)))
+        host = np.ctypeslib.as_array((C.c_double * (3 * N)).from_address(pinned.value)).reshape(m.data.shape)
+        host[...] = m.data
+        st = mx.SimState(mx.VectorField3(g, host))
+        sim = mx.Simulation(st, rhs, mx.IntegratorSpec("rk4", dt), sample_every=1,
+                            energy_in_samples=False)
+        sim.CHUNK = 1
+        t0 = time.perf_counter()
+        sim.run_until(mx.StopCondition(max_steps=args.steps))
+        el = time.perf_counter() - t0
+        e2e = {"value": N * args.steps / el, "unit": "cell-steps/s",
+               "h2d_bytes_per_step": int(24 * N / args.steps),
+               "d2h_bytes_per_step": int(24 * N / args.steps + 24),
+               "note": "Simulation.run_until from pinned host state; <m> read back every step"}
+        del st, sim
+        L.load().mxb_host_free(pinned)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cs, el, cores = cpu_reference(args.cpu_n, 2, 0)
+        cpu = {"value": cs, "unit": "cell-steps/s", "cores": cores, "kind": "port",
+               "sample": f"synthetic {args.cpu_n}^3 full H_eff, 2 RK4 steps, oracle numpy/scipy "
+                         f"(tensor build excluded)"}
+    if rank != 0:
+        return
+    out = {
+        "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"synthetic random-m {args.n}^3, full H_eff "
+                               "(demag+exchange+DMI+uniaxial anis+Zeeman), RK4",
+                   "cells": N, "dt": dt, "l2": "inputs (3.2 GB/field) > L2, no flush",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm,
+                     "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                     "peak_source": which},
+        "step_roofline": {"bytes_per_step": step_bytes,
+                          "achieved_GBs": step_bytes / (t_step * 1e-3) / 1e9,
+                          "frac": step_bytes / (t_step * 1e-3) / 1e9 / hbm},
+        "kernels_ms_per_step": share,
+        "demag_ms_per_eval": ms_eval.value, "cufft_demag_ms_per_eval": ms_cufft.value,
+        "tensor_build_s": t_build,
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(nl.value),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

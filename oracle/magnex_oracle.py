@@ -441,7 +441,7 @@ def kernel_spectra(packed: np.ndarray, workers: int = 1) -> np.ndarray:
                      for c in range(6)])
 
 
-def demag_field(spectra: np.ndarray, m: np.ndarray, workers: int = 1) -> np.ndarray:
+def demag_field(spectra: np.ndarray, m: np.ndarray, workers: int | None = None) -> np.ndarray:
     """Zero-padded FFT convolution H = N * M (demag.py:203-216)."""
     _, nz, ny, nx = m.shape
     pad = padded_dims(nx, ny, nz)

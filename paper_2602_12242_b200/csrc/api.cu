@@ -250,17 +250,19 @@ int mxb_demag_build(mxb_demag* d, int symmetric) {
     const size_t per = (size_t)p.pz * p.py * p.px;
     const size_t lat = (size_t)(2 * g.nx + 1) * (2 * g.ny + 1) * (2 * g.nz + 1);
     double *P = nullptr, *F = nullptr;
-    MXB_CUDA(cudaMalloc(&P, 6 * per * sizeof(double)));
+    MXB_CUDA(cudaMalloc(&P, per * sizeof(double)));
     cudaError_t e = cudaMalloc(&F, lat * sizeof(double));
     if (e != cudaSuccess) { cudaFree(P); return cuda_fail(e, "lattice", __FILE__, __LINE__); }
     int rc = MXB_OK;
-    for (int c = 0; c < 6 && !rc; ++c) rc = newell_packed_component(g, c, symmetric, P + c * per, F, d->st);
-    cudaFree(F);   // stream-ordered free is not needed: sync below before reuse
-    if (!rc) {
-        cudaMemsetAsync(p.K, 0, (size_t)p.pz * p.py * p.hxp * 6 * sizeof(double2), d->st);
-        rc = p.spectra_from_packed_dev(P, d->st);
+    cudaMemsetAsync(p.K, 0, (size_t)p.pz * p.py * p.hxp * 6 * sizeof(double2), d->st);
+    // one component at a time: lattice -> packed component -> x transform into K[..][c]
+    for (int c = 0; c < 6 && !rc; ++c) {
+        rc = newell_packed_component(g, c, symmetric, P, F, d->st);
+        if (!rc) rc = p.spectra_x_component(P, c, d->st);
     }
+    if (!rc) rc = p.spectra_yz(d->st);
     cudaStreamSynchronize(d->st);
+    cudaFree(F);
     cudaFree(P);
     if (rc) return rc;
     MXB_CUDA(cudaGetLastError());
@@ -665,27 +667,30 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
 // measurement helpers
 // ---------------------------------------------------------------------------
 int mxb_time_demag(mxb_ctx* c, mxb_demag* d, int iters, double* ms_eval, double* ms_pass5) {
-    if (!c || !d || !c->state_valid) { set_error("need ctx, demag and a resident state"); return MXB_EINVAL; }
+    if (!c || !d || !c->state_valid || iters < 1) { set_error("need ctx, demag and a resident state"); return MXB_EINVAL; }
     cudaSetDevice(c->dev);
     int rc = check_demag(c, d);
     if (rc) return rc;
     if ((rc = ensure_state(c))) return rc;
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    cudaEvent_t ev[6];
+    for (auto& e : ev) cudaEventCreate(&e);
     for (int w = 0; w < 2; ++w)
         if ((rc = demag_into(c, d, c->Yb[c->cur], c->Hd, nullptr))) return rc;
-    cudaEventRecord(e0, c->st);
-    for (int i = 0; i < iters; ++i)
-        if ((rc = demag_into(c, d, c->Yb[c->cur], c->Hd, nullptr))) return rc;
-    cudaEventRecord(e1, c->st);
-    MXB_CUDA(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    *ms_eval = ms / iters;
-    if (ms_pass5) *ms_pass5 = 0.0;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    double acc[5] = {0, 0, 0, 0, 0}, tot = 0;
+    for (int i = 0; i < iters; ++i) {
+        if ((rc = d->plan.field_dev(c->Yb[c->cur], c->Hd, c->st, nullptr, ev))) return rc;
+        MXB_CUDA(cudaEventSynchronize(ev[5]));
+        float ms = 0;
+        for (int p = 0; p < 5; ++p) {
+            cudaEventElapsedTime(&ms, ev[p], ev[p + 1]);
+            acc[p] += ms;
+        }
+        cudaEventElapsedTime(&ms, ev[0], ev[5]);
+        tot += ms;
+    }
+    *ms_eval = tot / iters;
+    if (ms_pass5) for (int p = 0; p < 5; ++p) ms_pass5[p] = acc[p] / iters;
+    for (auto& e : ev) cudaEventDestroy(e);
     return MXB_OK;
 }
 

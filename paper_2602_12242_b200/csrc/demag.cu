@@ -58,7 +58,8 @@ int make_plan(int L, int dev, Plan1D* p, double2** tw_owned) {
 // zero-padded to L, forward FFT, first hx bins -> out[(row*hxp+kx)*nc + c].
 __global__ void k_rows_r2c(const double* __restrict__ in, long long in_cstride, int in_pitch,
                            int n_in, double2* __restrict__ out, int hxp, int hx, int nc,
-                           int nrows, Plan1D p, int NL, const int* __restrict__ halt) {
+                           int ostride, int coff, int nrows, Plan1D p, int NL,
+                           const int* __restrict__ halt) {
     if (halt && *halt) return;
     extern __shared__ double2 sm[];
     const int L = p.L, ld = L + 1;
@@ -87,7 +88,7 @@ __global__ void k_rows_r2c(const double* __restrict__ in, long long in_cstride, 
         const int kx = q / nc, c = q - kx * nc;
         const long long row = row0 + rl;
         if (row >= nrows) continue;
-        out[(row * hxp + kx) * nc + c] = r[(rl * nc + c) * ld + kx];
+        out[(row * hxp + kx) * ostride + coff + c] = r[(rl * nc + c) * ld + kx];
     }
 }
 
@@ -241,14 +242,15 @@ static size_t smem_for(int L, int NL) { return 2 * (size_t)NL * (L + 1) * sizeof
 
 int launch_rows_r2c(const Plan1D& p, const double* in, long long in_cstride, int in_pitch,
                     int n_in, double2* out, int hxp, int hx, int nc, long long nrows,
-                    cudaStream_t st, const int* halt) {
+                    cudaStream_t st, const int* halt, int ostride, int coff) {
+    if (ostride <= 0) ostride = nc;
     int NL = lines_per_block(p.L, nc);
     size_t sm = smem_for(p.L, NL);
     if (sm > kSmemMax) { set_error("x transform length too large for the generic path"); return MXB_EINVAL; }
     long long nlines = nrows * nc;
     unsigned nb = (unsigned)((nlines + NL - 1) / NL);
     k_rows_r2c<<<nb, kThreads, sm, st>>>(in, in_cstride, in_pitch, n_in, out, hxp, hx, nc,
-                                         (int)nrows, p, NL, halt);
+                                         ostride, coff, (int)nrows, p, NL, halt);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
@@ -333,11 +335,15 @@ void DemagPlan::release() {
     X1 = X2 = K = nullptr;
 }
 
-// 6 forward transforms of a packed (6,pz,py,px) device tensor into K.
-int DemagPlan::spectra_from_packed_dev(const double* P, cudaStream_t st) {
+// x r2c of one packed real-space component (pz,py,px) into slot c of K
+int DemagPlan::spectra_x_component(const double* Pc, int c, cudaStream_t st) {
     const long long plane = (long long)pz * py;
-    int rc = launch_rows_r2c(plx, P, plane * px, px, px, K, hxp, hx, 6, plane, st, nullptr);
-    if (rc) return rc;
+    return launch_rows_r2c(plx, Pc, 0, px, px, K, hxp, hx, 1, plane, st, nullptr, 6, c);
+}
+
+// y and z forward transforms of all 6 slots of K, in place
+int DemagPlan::spectra_yz(cudaStream_t st) {
+    int rc;
     if (py > 1) {
         // y lines: element stride hxp*6, Q = hxp*6 per z-plane
         rc = launch_lines(-1, ply, K, K, py, py, (long long)hxp * 6, (long long)hxp * 6, hxp * 6,
@@ -354,39 +360,64 @@ int DemagPlan::spectra_from_packed_dev(const double* P, cudaStream_t st) {
     return MXB_OK;
 }
 
-int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt) {
+// 6 forward transforms of a packed (6,pz,py,px) device tensor into K.
+int DemagPlan::spectra_from_packed_dev(const double* P, cudaStream_t st) {
+    const long long per = (long long)pz * py * px;
+    for (int c = 0; c < 6; ++c) {
+        int rc = spectra_x_component(P + c * per, c, st);
+        if (rc) return rc;
+    }
+    return spectra_yz(st);
+}
+
+int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
+                         cudaEvent_t* ev) {
+    auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
     if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
     const long long N = g.N;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     int rc;
+    mark(0);
     // P1
-    rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, (long long)nz * ny, st, halt);
+    rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, (long long)nz * ny, st, halt, 3, 0);
     if (rc) return rc;
+    mark(1);
     const long long row = (long long)hxp * 3;   // complex elements per (z,y) row
     if (pz > 1) {
         if (py > 1) {
             // P2: y forward, per z-plane: ny rows in -> py rows out
-            rc = launch_lines(-1, ply, X1, X2, ny, py, row, row, (int)row, (long long)nz * row,
+            rc = launch_lines(-1, ply, X1, X2, ny, py, row, row, hx * 3, (long long)nz * hx * 3,
                               (long long)ny * row, (long long)py * row, st, halt);
             if (rc) return rc;
         }
+        mark(2);
         // P3 along z: line base = ky*row + kx*3 + c, element stride py*row
         rc = launch_fused(plz, X2, K, nz, (long long)py * row, hx, hxp, py, row, scale, st, halt);
         if (rc) return rc;
+        mark(3);
         if (py > 1) {
-            rc = launch_lines(1, ply, X2, X1, py, ny, row, row, (int)row, (long long)nz * row,
+            rc = launch_lines(1, ply, X2, X1, py, ny, row, row, hx * 3, (long long)nz * hx * 3,
                               (long long)py * row, (long long)ny * row, st, halt);
             if (rc) return rc;
         }
+        mark(4);
     } else if (py > 1) {
+        mark(2);
         rc = launch_fused(ply, X1, K, ny, row, hx, hxp, 1, 0, scale, st, halt);
         if (rc) return rc;
+        mark(3);
+        mark(4);
     } else {
+        mark(2);
         rc = launch_fused(plz, X1, K, 1, row, hx, hxp, 1, 0, scale, st, halt);
         if (rc) return rc;
+        mark(3);
+        mark(4);
     }
     // P5
-    return launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, (long long)nz * ny, st, halt);
+    rc = launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, (long long)nz * ny, st, halt);
+    mark(5);
+    return rc;
 }
 
 }  // namespace mxb

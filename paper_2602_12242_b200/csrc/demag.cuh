@@ -21,13 +21,17 @@ struct DemagPlan {
     int init(const mxb_grid& g, int device);
     void release();
     int spectra_from_packed_dev(const double* P, cudaStream_t st);
-    int field_dev(const double* m, double* h, cudaStream_t st, const int* halt);
+    int spectra_x_component(const double* Pc, int c, cudaStream_t st);
+    int spectra_yz(cudaStream_t st);
+    // ev (optional): 6 events recorded before P1 and after each of the 5 passes
+    int field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
+                  cudaEvent_t* ev = nullptr);
 };
 
 int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);
 int launch_rows_r2c(const Plan1D& p, const double* in, long long in_cstride, int in_pitch,
                     int n_in, double2* out, int hxp, int hx, int nc, long long nrows,
-                    cudaStream_t st, const int* halt);
+                    cudaStream_t st, const int* halt, int ostride = 0, int coff = 0);
 int launch_lines(int dir, const Plan1D& p, const double2* in, double2* out, int n_in, int n_out,
                  long long ES_in, long long ES_out, int Q, long long nlines, long long OS_in,
                  long long OS_out, cudaStream_t st, const int* halt);

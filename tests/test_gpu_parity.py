@@ -83,9 +83,20 @@ def test_heff_rhs_and_steps(name, mode):
     got = np.array([e.e_demag, e.e_exch, e.e_anis, e.e_zeeman])
     assert np.all(np.abs(got - ref) <= 1e-12 * np.maximum(np.abs(ref), 1e-30) + 1e-30), (got, ref)
     # one full step through the device loop (RK4 with stage renorm, and Euler)
+    omat = mat_of(z)
     for method, key in (("rk4", "rk4_step"), ("euler", "euler_step")):
         st = mx.SimState(mx.VectorField3(g, m0.copy()))
         sim = mx.Simulation(st, rhs, mx.IntegratorSpec(method, dt), energy_in_samples=False)
+        y = z[key]
+        mask = omat.mask
+        nr = np.sqrt(np.einsum("cijk,cijk->ijk", y, y))[mask]
+        drift = float(np.max(np.abs(nr / omat.Ms[mask] - 1.0)))
+        if drift > 0.1:   # the reference driver would raise here (llg.py:348-353)
+            with pytest.raises(mx.IntegrationBlowup) as ei:
+                sim.run_until(mx.StopCondition(max_steps=1))
+            assert ei.value.step == 1 and abs(ei.value.drift - drift) <= 1e-12 * drift
+            assert np.array_equal(st.m.data, m0)   # state is left at the last good step
+            continue
         sim.run_until(mx.StopCondition(max_steps=1))
         # the driver renormalises after the step (llg.py:355)
         ref_step = O.renormalize(z[key], mat_of(z))
