@@ -23,6 +23,7 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
     snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
              cudaGetErrorString(e), what, file, line);
     g_err = buf;
+    cudaGetLastError();   // clear non-sticky errors (e.g. a failed allocation)
     return MXB_ECUDA;
 }
 

@@ -79,6 +79,10 @@ extern "C" int mxb_time_demag_cufft(mxb_demag* d, int iters, double* ms_eval) {
     const Grid& g = p.g;
     const long long real_n = (long long)p.px * p.py * p.pz;
     const long long spec_n = (long long)p.pz * p.py * p.hx;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (3 * g.N * 2 + 3 * real_n) * sizeof(double) + 9 * spec_n * sizeof(double2);
+    if (need * 3 / 2 > fr) { set_error("not enough free memory for the cuFFT comparison"); return MXB_EINVAL; }
     double *m = nullptr, *h = nullptr, *pad = nullptr;
     double2 *spec = nullptr, *Ks = nullptr;
     MXB_CUDA(cudaMalloc(&m, 3 * g.N * sizeof(double)));
