@@ -134,6 +134,9 @@ int mxb_demag_field(mxb_demag* d, const double* m, double* h);
  * fields resident */
 int mxb_demag_field_dev(mxb_demag* d, const double* m_dev, double* h_dev);
 size_t mxb_demag_bytes(mxb_demag* d);
+/* select the register-resident radix-16 kernels (1, default) or the generic
+ * mixed-radix shared-memory kernels (0) where both cover the shape */
+int mxb_demag_set_fast(mxb_demag* d, int fast);
 
 /* ---- local operators and assembly (host buffers) ----------------------- */
 /* ExchangeOperator / DmiOperator / AnisotropyOperator .__call__

@@ -266,6 +266,8 @@ int mxb_demag_build(mxb_demag* d, int symmetric) {
     cudaFree(F);
     cudaFree(P);
     if (rc) return rc;
+    // the mirrored tensor has exactly real, parity-structured spectra
+    if (symmetric && (rc = p.quarterize(d->st))) return rc;
     MXB_CUDA(cudaGetLastError());
     return MXB_OK;
 }
@@ -296,19 +298,53 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     DemagPlan& p = d->plan;
     if (!p.has_kernel) { set_error("no spectra"); return MXB_EINVAL; }
     cudaSetDevice(p.dev);
-    const size_t n = (size_t)p.pz * p.py * p.hxp * 6;
-    std::vector<double2> h(n);
-    MXB_CUDA(cudaMemcpy(h.data(), p.K, n * sizeof(double2), cudaMemcpyDeviceToHost));
-    // [kz][ky][kx][6] -> (6, pz, py, hx) interleaved
+    if (p.kmode == 0) {
+        const size_t n = (size_t)p.pz * p.py * p.hxp * 6;
+        std::vector<double2> h(n);
+        MXB_CUDA(cudaMemcpy(h.data(), p.K, n * sizeof(double2), cudaMemcpyDeviceToHost));
+        // [kz][ky][kx][6] -> (6, pz, py, hx) interleaved
+        for (int c = 0; c < 6; ++c)
+            for (int kz = 0; kz < p.pz; ++kz)
+                for (int ky = 0; ky < p.py; ++ky)
+                    for (int kx = 0; kx < p.hx; ++kx) {
+                        const double2 v = h[(((size_t)kz * p.py + ky) * p.hxp + kx) * 6 + c];
+                        const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
+                        out[2 * o] = v.x;
+                        out[2 * o + 1] = v.y;
+                    }
+        return MXB_OK;
+    }
+    // quarter storage: unfold with the parity signs
+    const int L = p.fused_L(), G = p.fused_G();
+    const int L2 = L / 2 + 1, G2 = G / 2 + 1;
+    const bool e_is_z = p.pz > 1 || p.py == 1;
+    const size_t n = (size_t)L2 * G2 * p.hxp * 6;
+    std::vector<double> h(n);
+    MXB_CUDA(cudaMemcpy(h.data(), p.Kq, n * sizeof(double), cudaMemcpyDeviceToHost));
     for (int c = 0; c < 6; ++c)
         for (int kz = 0; kz < p.pz; ++kz)
-            for (int ky = 0; ky < p.py; ++ky)
+            for (int ky = 0; ky < p.py; ++ky) {
+                const int e = e_is_z ? kz : ky, g = e_is_z ? ky : kz;
+                const bool re = 2 * e > L, rg = 2 * g > G;
+                const int e2 = re ? L - e : e, g2 = rg ? G - g : g;
+                const bool fy = e_is_z ? rg : re, fz = e_is_z ? re : rg;
+                double sgn = 1.0;
+                if (c == 1 && fy) sgn = -1.0;
+                if (c == 2 && fz) sgn = -1.0;
+                if (c == 4 && (fy != fz)) sgn = -1.0;
                 for (int kx = 0; kx < p.hx; ++kx) {
-                    const double2 v = h[(((size_t)kz * p.py + ky) * p.hxp + kx) * 6 + c];
+                    const double v = sgn * h[(((size_t)e2 * G2 + g2) * p.hxp + kx) * 6 + c];
                     const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
-                    out[2 * o] = v.x;
-                    out[2 * o + 1] = v.y;
+                    out[2 * o] = v;
+                    out[2 * o + 1] = 0.0;
                 }
+            }
+    return MXB_OK;
+}
+
+int mxb_demag_set_fast(mxb_demag* d, int fast) {
+    if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    d->plan.fast = fast != 0;
     return MXB_OK;
 }
 

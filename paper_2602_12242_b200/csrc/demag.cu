@@ -316,6 +316,7 @@ int DemagPlan::init(const mxb_grid& gr, int device) {
     if ((rc = make_plan(px, dev, &plx, &tw[0]))) return rc;
     if ((rc = make_plan(py, dev, &ply, &tw[1]))) return rc;
     if ((rc = make_plan(pz, dev, &plz, &tw[2]))) return rc;
+    if (px >= 4 && (rc = make_plan(px / 2, dev, &plm, &twm))) return rc;
     size_t x1 = (size_t)g.nz * g.ny * hxp * 3;
     size_t x2 = (size_t)g.nz * py * hxp * 3;
     MXB_CUDA(cudaMalloc(&X1, x1 * sizeof(double2)));
@@ -329,6 +330,10 @@ int DemagPlan::init(const mxb_grid& gr, int device) {
 void DemagPlan::release() {
     cudaSetDevice(dev);
     for (auto& t : tw) if (t) cudaFree(t);
+    if (twm) cudaFree(twm);
+    if (Kq) cudaFree(Kq);
+    Kq = nullptr;
+    twm = nullptr;
     if (X2 && X2 != X1) cudaFree(X2);
     if (X1) cudaFree(X1);
     if (K) cudaFree(K);
@@ -376,48 +381,100 @@ int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int*
     if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
     const long long N = g.N;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const long long rows = (long long)nz * ny;
+    const bool fast_x = fast && px >= 4 && (nx % 2) == 0;
     int rc;
     mark(0);
-    // P1
-    rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, (long long)nz * ny, st, halt, 3, 0);
+    // P1: x r2c
+    rc = -1;
+    if (fast_x) rc = fast_rows(true, px / 2, m, X1, nullptr, N, nx, nx / 2, hxp, rows, plm.tw, plx.tw, st, halt);
+    if (rc == -1) rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, rows, st, halt, 3, 0);
     if (rc) return rc;
     mark(1);
     const long long row = (long long)hxp * 3;   // complex elements per (z,y) row
+    auto cols = [&](int dir, const double2* in, double2* out, int n_in, int n_out, long long OS_in,
+                    long long OS_out) {
+        int r = -1;
+        if (fast) r = fast_cols(dir, py, in, out, n_in, n_out, row, row, hx * 3, (long long)nz * hx * 3,
+                                OS_in, OS_out, ply.tw, st, halt);
+        if (r == -1) r = launch_lines(dir, ply, in, out, n_in, n_out, row, row, hx * 3,
+                                      (long long)nz * hx * 3, OS_in, OS_out, st, halt);
+        return r;
+    };
+    auto fused = [&](const Plan1D& pl, double2* X, int n, long long ES, int G, long long GS, int e_is_z) {
+        int r = -1;
+        if (fast || kmode != 0) {
+            FusedArgs a{X, kmode == 0 ? (const void*)K : (const void*)Kq, n, ES, hx, hxp, G, GS, scale, e_is_z};
+            r = fast_fused(pl.L, kmode, a, pl.tw, st, halt);
+        }
+        if (r == -1 && kmode == 0) r = launch_fused(pl, X, K, n, ES, hx, hxp, G, GS, scale, st, halt);
+        if (r == -1) { set_error("no fused kernel for this shape"); r = MXB_EINVAL; }
+        return r;
+    };
     if (pz > 1) {
         if (py > 1) {
             // P2: y forward, per z-plane: ny rows in -> py rows out
-            rc = launch_lines(-1, ply, X1, X2, ny, py, row, row, hx * 3, (long long)nz * hx * 3,
-                              (long long)ny * row, (long long)py * row, st, halt);
-            if (rc) return rc;
+            if ((rc = cols(-1, X1, X2, ny, py, (long long)ny * row, (long long)py * row))) return rc;
         }
         mark(2);
         // P3 along z: line base = ky*row + kx*3 + c, element stride py*row
-        rc = launch_fused(plz, X2, K, nz, (long long)py * row, hx, hxp, py, row, scale, st, halt);
-        if (rc) return rc;
+        if ((rc = fused(plz, X2, nz, (long long)py * row, py, row, 1))) return rc;
         mark(3);
         if (py > 1) {
-            rc = launch_lines(1, ply, X2, X1, py, ny, row, row, hx * 3, (long long)nz * hx * 3,
-                              (long long)py * row, (long long)ny * row, st, halt);
-            if (rc) return rc;
+            if ((rc = cols(1, X2, X1, py, ny, (long long)py * row, (long long)ny * row))) return rc;
         }
         mark(4);
     } else if (py > 1) {
         mark(2);
-        rc = launch_fused(ply, X1, K, ny, row, hx, hxp, 1, 0, scale, st, halt);
-        if (rc) return rc;
+        if ((rc = fused(ply, X1, ny, row, 1, 0, 0))) return rc;
         mark(3);
         mark(4);
     } else {
         mark(2);
-        rc = launch_fused(plz, X1, K, 1, row, hx, hxp, 1, 0, scale, st, halt);
-        if (rc) return rc;
+        if ((rc = fused(plz, X1, 1, row, 1, 0, 1))) return rc;
         mark(3);
         mark(4);
     }
-    // P5
-    rc = launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, (long long)nz * ny, st, halt);
+    // P5: x c2r
+    rc = -1;
+    if (fast_x) rc = fast_rows(false, px / 2, nullptr, X1, h, N, nx, nx / 2, hxp, rows, plm.tw, plx.tw, st, halt);
+    if (rc == -1) rc = launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, rows, st, halt);
     mark(5);
     return rc;
+}
+
+// real parts of the (exactly real, parity-structured) spectra, quarter storage
+__global__ void k_quarterize(const double2* K, double* Kq, int L, int G, int py, int hxp,
+                             int e_is_z) {
+    const int L2 = L / 2 + 1, G2 = G / 2 + 1;
+    const long long tot = (long long)L2 * G2 * hxp * 6;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(t % 6);
+        long long r = t / 6;
+        const int kx = (int)(r % hxp);
+        r /= hxp;
+        const int g2 = (int)(r % G2), e2 = (int)(r / G2);
+        const int kz = e_is_z ? e2 : g2, ky = e_is_z ? g2 : e2;
+        Kq[t] = K[(((long long)kz * py + ky) * hxp + kx) * 6 + c].x;
+    }
+}
+
+int DemagPlan::quarterize(cudaStream_t st) {
+    const int L = fused_L(), G = fused_G();
+    if (!fast_fused_ok(L)) return MXB_OK;   // keep complex spectra for the generic path
+    const int e_is_z = pz > 1 ? 1 : (py > 1 ? 0 : 1);
+    const size_t n = (size_t)(L / 2 + 1) * (G / 2 + 1) * hxp * 6;
+    MXB_CUDA(cudaMalloc(&Kq, n * sizeof(double)));
+    k_quarterize<<<148 * 8, 256, 0, st>>>(K, Kq, L, G, py, hxp, e_is_z);
+    MXB_LAUNCH_CHECK();
+    MXB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(K);
+    K = nullptr;
+    kmode = 2;
+    bytes -= (size_t)pz * py * hxp * 6 * sizeof(double2);
+    bytes += n * sizeof(double);
+    return MXB_OK;
 }
 
 }  // namespace mxb

@@ -5,6 +5,27 @@
 
 namespace mxb {
 
+struct FusedArgs {
+    double2* X;
+    const void* K;
+    int n;
+    long long ES;
+    int hx, hxp, G;
+    long long GS;
+    double scale;
+    int e_is_z;   // the transformed axis: 1 -> z (3-D), 0 -> y (film)
+};
+
+int fast_cols(int dir, int L, const double2* in, double2* out, int n_in, int n_out,
+              long long ES_in, long long ES_out, int Q, long long nlines, long long OS_in,
+              long long OS_out, const double2* tw, cudaStream_t st, const int* halt);
+bool fast_fused_ok(int L);
+int fast_fused(int L, int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
+               const int* halt);
+int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, long long cstride,
+              int pitch, int nhalf, int hxp, long long nrows, const double2* twM,
+              const double2* tw2M, cudaStream_t st, const int* halt);
+
 struct DemagPlan {
     int dev = 0;
     Grid g{};
@@ -14,8 +35,16 @@ struct DemagPlan {
     double2* tw[3] = {nullptr, nullptr, nullptr};
     double2* X1 = nullptr;   // [nz][ny][hxp][3]
     double2* X2 = nullptr;   // [nz][py][hxp][3]
-    double2* K = nullptr;    // [pz][py][hxp][6] spectra (unscaled)
+    double2* K = nullptr;    // [pz][py][hxp][6] spectra (unscaled), complex
+    double* Kq = nullptr;    // parity-reduced real spectra [L/2+1][G/2+1][hxp][6]
+    int kmode = 0;           // 0 complex K, 2 real quarter Kq
+    Plan1D plm{};            // length px/2 (fast x rows)
+    double2* twm = nullptr;
+    bool fast = true;        // use the register-resident kernels where shapes allow
     bool has_kernel = false;
+    int fused_L() const { return pz > 1 ? pz : (py > 1 ? py : 1); }
+    int fused_G() const { return pz > 1 ? py : 1; }
+    int quarterize(cudaStream_t st);
     size_t bytes = 0;
 
     int init(const mxb_grid& g, int device);

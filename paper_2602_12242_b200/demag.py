@@ -94,6 +94,11 @@ class DemagKernel:
         L.check(L.load().mxb_demag_get_spectra(self._d.h, L.dptr(out)), "get_spectra")
         return out[..., 0] + 1j * out[..., 1]
 
+    def set_fast(self, flag: bool) -> None:
+        """Use the register-resident radix-16 kernels (default) or the generic
+        mixed-radix kernels where both cover the shape."""
+        L.check(L.load().mxb_demag_set_fast(self._d.h, 1 if flag else 0), "set_fast")
+
     @property
     def device_bytes(self) -> int:
         return int(L.load().mxb_demag_bytes(self._d.h))
