@@ -20,8 +20,9 @@ template <int L> struct Cfg {
     static constexpr int TPL = L / R;
     // columns: ~256 threads, at least 2 lines (32-byte segments)
     static constexpr int NLc = (256 * R / L) >= 2 ? (256 * R / L) : 2;
-    // fused: NK kx columns x 3 components
-    static constexpr int NKf = (256 * R / (3 * L)) >= 2 ? (256 * R / (3 * L)) : 2;
+    // fused: NK kx columns x 3 components (one kx column for long lines, so
+    // two or three CTAs share an SM and overlap their load/compute phases)
+    static constexpr int NKf = L >= 512 ? 1 : ((256 * R / (3 * L)) >= 2 ? (256 * R / (3 * L)) : 2);
     // rows (M = L complex points per row): NR rows x 3 components
     static constexpr int NRr = (256 * R / (3 * L)) >= 1 ? (256 * R / (3 * L)) : 1;
 };
@@ -30,7 +31,7 @@ template <int L> struct Cfg {
 // strided columns (y passes)
 // ---------------------------------------------------------------------------
 template <int L, int DIR>
-__global__ void __launch_bounds__(Cfg<L>::NLc * Cfg<L>::TPL)
+__global__ void __launch_bounds__(Cfg<L>::NLc * Cfg<L>::TPL, 2)
 k_col_fast(const double2* in, double2* out, int n_in, int n_out, long long ES_in, long long ES_out,
            int Q, long long nlines, long long OS_in, long long OS_out,
            const double2* __restrict__ tw, const int* __restrict__ halt) {
@@ -94,7 +95,7 @@ __device__ __forceinline__ void kernel6(const FusedArgs& a, int L, int e, int g,
 }
 
 template <int L, int KMODE>
-__global__ void __launch_bounds__(3 * Cfg<L>::NKf * Cfg<L>::TPL)
+__global__ void __launch_bounds__(3 * Cfg<L>::NKf * Cfg<L>::TPL, 2)
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<L>::R, TPL = Cfg<L>::TPL, NK = Cfg<L>::NKf, NL = 3 * NK;
@@ -156,7 +157,7 @@ k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict_
 // x rows: r2c of real length 2M through a complex FFT of length M
 // ---------------------------------------------------------------------------
 template <int M>
-__global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL)
+__global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
 k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in2,
            double2* __restrict__ out, int hxp, long long nrows, const double2* __restrict__ twM,
            const double2* __restrict__ tw2M, const int* __restrict__ halt) {
@@ -198,7 +199,7 @@ k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in
 }
 
 template <int M>
-__global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL)
+__global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
 k_c2r_fast(const double2* __restrict__ X, int hxp, double* __restrict__ out, long long cstride,
            int pitch, int n_out2, long long nrows, const double2* __restrict__ twM,
            const double2* __restrict__ tw2M, const int* __restrict__ halt) {

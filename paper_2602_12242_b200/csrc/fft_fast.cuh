@@ -127,8 +127,16 @@ __device__ __forceinline__ void stages(double2 (&v)[R], double2* s, int b, int t
         for (int q = 0; q < NQ; ++q) {
             const int j = t + q * TPL;
             const int k = j & (Ns - 1);
+            // twiddles w^m: load the powers of two, build the rest with <= 3 products
+            double2 w[r];
+            w[0] = make_double2(1.0, 0.0);
 #pragma unroll
-            for (int m = 1; m < r; ++m) v[q * r + m] = cmul(v[q * r + m], twid<DIR>(tw, k * m * TS));
+            for (int p = 1; p < r; p <<= 1) w[p] = twid<DIR>(tw, k * p * TS);
+#pragma unroll
+            for (int m = 3; m < r; ++m)
+                if (m & (m - 1)) w[m] = cmul(w[m & (m - 1)], w[m & -m]);
+#pragma unroll
+            for (int m = 1; m < r; ++m) v[q * r + m] = cmul(v[q * r + m], w[m]);
             DFT<r, DIR>::run(&v[q * r]);
         }
         if constexpr (Ns * r < L) {
