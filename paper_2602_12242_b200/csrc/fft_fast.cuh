@@ -9,7 +9,7 @@
 //
 // Shared layout: COL (lines fastest, used for strided columns) puts element
 // e of line b at pad(e)*NL + b; ROW (used for contiguous x rows) at
-// b*(L + L/R) + pad(e).  pad(e) = e + e/R keeps every access pattern of the
+// b*(L + L/R + 1) + pad(e).  pad(e) = e + e/R keeps every access pattern of the
 // stages bank-conflict free for 16-byte elements.
 #pragma once
 
@@ -94,11 +94,21 @@ __device__ __forceinline__ int sidx(int b, int e) {
     constexpr int LOGR = ilog2(R);
     const int pe = e + (e >> LOGR);
     if (COL) return pe * NL + b;
-    return b * (L + L / R) + pe;
+    return b * (L + L / R + 1) + pe;   // +1: successive lines start in different banks
 }
 
 template <int L, int R, int NL>
-__host__ __device__ constexpr int smem_elems() { return NL * (L + L / R); }
+__host__ __device__ constexpr int smem_elems() { return NL * (L + L / R + 1); }
+
+// cp.async 16-byte global -> shared copy; pred=false zero-fills (src-size 0)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // element index held by register i after the final stage
 template <int L, int R>
