@@ -9,6 +9,8 @@
 //             for films); the kernel rows of the tile are staged in shared
 //             memory too, in parity-reduced (quarter) or complex storage.
 // Same buffer layouts as the generic kernels in demag.cu.
+#include <stdlib.h>
+
 #include <map>
 #include <mutex>
 #include <set>
@@ -21,8 +23,8 @@ namespace mxb {
 
 using namespace ff;
 
-template <int L> struct Cfg {
-    static constexpr int R = L >= 16 ? 16 : (L < 1 ? 1 : L);
+template <int L, int RMAX = 16> struct Cfg {
+    static constexpr int R = L >= RMAX ? RMAX : (L < 1 ? 1 : L);
     static constexpr int TPL = L / R;
     // columns: ~256 threads, at least 2 lines (32-byte segments)
     static constexpr int NLc = (256 * R / L) >= 2 ? (256 * R / L) : 2;
@@ -45,11 +47,11 @@ struct ColArgs {
     long long nlines, OS_in, OS_out;
 };
 
-template <int L, int DIR>
-__global__ void __launch_bounds__(Cfg<L>::NLc * Cfg<L>::TPL, 2)
+template <int L, int DIR, int RM>
+__global__ void __launch_bounds__(Cfg<L, RM>::NLc * Cfg<L, RM>::TPL, 2)
 k_col_fast(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
-    constexpr int R = Cfg<L>::R, TPL = Cfg<L>::TPL, NL = Cfg<L>::NLc;
+    constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NL = Cfg<L, RM>::NLc;
     extern __shared__ double2 sm[];
     double2* X = sm;
     double2* S = sm + smem_elems<L, R, NL>();
@@ -105,11 +107,11 @@ __device__ __forceinline__ int g_of(int r, int G) {
     return (r & 1) ? (r + 1) / 2 : G - r / 2;
 }
 
-template <int L, int KMODE>
-__global__ void __launch_bounds__(3 * Cfg<L>::NKf * Cfg<L>::TPL, 2)
+template <int L, int KMODE, int RM>
+__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, 2)
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
-    constexpr int R = Cfg<L>::R, TPL = Cfg<L>::TPL, NK = Cfg<L>::NKf, NL = 3 * NK;
+    constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
     constexpr int KROWS = KMODE == 2 ? (L / 2 + 1) : L;
     constexpr int KCH = KMODE == 2 ? 3 : 6;   // 16-byte chunks per (row, kx)
     extern __shared__ double2 sm[];
@@ -373,6 +375,7 @@ static int persistent_grid(F f, int threads, size_t smem, long long ntiles, int*
     std::lock_guard<std::mutex> lk(mu);
     if (!attr_done.count((const void*)f)) {
         MXB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFastSmemMax));
+        MXB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr_done.insert((const void*)f);
     }
     auto key = std::make_pair((const void*)f, smem);
@@ -390,43 +393,43 @@ static int persistent_grid(F f, int threads, size_t smem, long long ntiles, int*
     return MXB_OK;
 }
 
-template <int L>
+template <int L, int RM>
 static int col_launch(int dir, const ColArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
-    constexpr int R = Cfg<L>::R, NL = Cfg<L>::NLc;
+    constexpr int R = Cfg<L, RM>::R, NL = Cfg<L, RM>::NLc;
     const size_t sm = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n_in) * sizeof(double2);
     if (sm > kFastSmemMax) return -1;
     const long long ntiles = (a.nlines + NL - 1) / NL;
-    const int thr = NL * Cfg<L>::TPL;
+    const int thr = NL * Cfg<L, RM>::TPL;
     int grid = 0, rc;
     if (dir < 0) {
-        if ((rc = persistent_grid(k_col_fast<L, -1>, thr, sm, ntiles, &grid))) return rc;
-        k_col_fast<L, -1><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_col_fast<L, -1, RM>, thr, sm, ntiles, &grid))) return rc;
+        k_col_fast<L, -1, RM><<<grid, thr, sm, st>>>(a, tw, halt);
     } else {
-        if ((rc = persistent_grid(k_col_fast<L, 1>, thr, sm, ntiles, &grid))) return rc;
-        k_col_fast<L, 1><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_col_fast<L, 1, RM>, thr, sm, ntiles, &grid))) return rc;
+        k_col_fast<L, 1, RM><<<grid, thr, sm, st>>>(a, tw, halt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
 
-template <int L>
+template <int L, int RM>
 static int fused_launch(int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
                         const int* halt) {
-    constexpr int R = Cfg<L>::R, NK = Cfg<L>::NKf, NL = 3 * NK;
+    constexpr int R = Cfg<L, RM>::R, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
     const int krows = kmode == 2 ? (L / 2 + 1) : L;
     const int kch = kmode == 2 ? 3 : 6;
     const size_t sm = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n + (size_t)krows * NK * kch) *
                       sizeof(double2);
     if (sm > kFastSmemMax) return -1;
     const long long ntiles = (long long)a.G * ((a.hx + NK - 1) / NK);
-    const int thr = NL * Cfg<L>::TPL;
+    const int thr = NL * Cfg<L, RM>::TPL;
     int grid = 0, rc;
     if (kmode == 2) {
-        if ((rc = persistent_grid(k_fused_fast<L, 2>, thr, sm, ntiles, &grid))) return rc;
-        k_fused_fast<L, 2><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_fused_fast<L, 2, RM>, thr, sm, ntiles, &grid))) return rc;
+        k_fused_fast<L, 2, RM><<<grid, thr, sm, st>>>(a, tw, halt);
     } else {
-        if ((rc = persistent_grid(k_fused_fast<L, 0>, thr, sm, ntiles, &grid))) return rc;
-        k_fused_fast<L, 0><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_fused_fast<L, 0, RM>, thr, sm, ntiles, &grid))) return rc;
+        k_fused_fast<L, 0, RM><<<grid, thr, sm, st>>>(a, tw, halt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
@@ -459,12 +462,27 @@ static int rows_launch(bool fwd, const double* in_r, double2* X, double* out_r, 
     MACRO(1024) MACRO(2048) MACRO(4096)
 
 // each returns -1 when the fast path does not cover the shape
+// radix of the register-resident kernels (MXB_COL_RADIX / MXB_FUSED_RADIX = 8 or 16)
+static int env_radix(const char* name, int dflt) {
+    const char* v = getenv(name);
+    if (!v) return dflt;
+    const int r = atoi(v);
+    return (r == 8 || r == 16) ? r : dflt;
+}
+static int col_radix() { static int r = env_radix("MXB_COL_RADIX", 16); return r; }
+static int fused_radix() { static int r = env_radix("MXB_FUSED_RADIX", 16); return r; }
+
 int fast_cols(int dir, int L, const double2* in, double2* out, int n_in, int n_out,
               long long ES_in, long long ES_out, int Q, long long nlines, long long OS_in,
               long long OS_out, const double2* tw, cudaStream_t st, const int* halt) {
     if (!pow2(L)) return -1;
     const ColArgs a{in, out, n_in, n_out, ES_in, ES_out, Q, nlines, OS_in, OS_out};
-#define CASE(V) case V: return col_launch<V>(dir, a, tw, st, halt);
+    if (col_radix() == 8) {
+#define CASE(V) case V: return col_launch<V, 8>(dir, a, tw, st, halt);
+        switch (L) { MXB_POW2_CASES(CASE) default: return -1; }
+#undef CASE
+    }
+#define CASE(V) case V: return col_launch<V, 16>(dir, a, tw, st, halt);
     switch (L) { MXB_POW2_CASES(CASE) default: return -1; }
 #undef CASE
 }
@@ -474,7 +492,16 @@ bool fast_fused_ok(int L) { return L == 1 || (pow2(L) && L <= 2048); }
 int fast_fused(int L, int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
                const int* halt) {
     if (!fast_fused_ok(L) || kmode == 1) return -1;
-#define CASE(V) case V: return fused_launch<V>(kmode, a, tw, st, halt);
+    if (fused_radix() == 8) {
+#define CASE(V) case V: return fused_launch<V, 8>(kmode, a, tw, st, halt);
+        switch (L) {
+            CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512)
+            CASE(1024) CASE(2048)
+            default: return -1;
+        }
+#undef CASE
+    }
+#define CASE(V) case V: return fused_launch<V, 16>(kmode, a, tw, st, halt);
     switch (L) {
         CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512)
         CASE(1024) CASE(2048)
