@@ -169,7 +169,7 @@ int mxb_ctx_create(const mxb_grid* gr, const mxb_material* m, int device, mxb_ct
     }
     c->dv = derive(md, c->g);
     e = cudaMalloc(&c->ctl, sizeof(Ctl));
-    if (e == cudaSuccess) e = cudaMalloc(&c->partials, sizeof(double) * kReduceSlots * 148 * 16);
+    if (e == cudaSuccess) e = cudaMalloc(&c->partials, sizeof(double) * kReduceSlots * (size_t)stage_blocks(c->g.N));
     if (e != cudaSuccess) { mxb_ctx_destroy(c); return cuda_fail(e, "ctl", __FILE__, __LINE__); }
     cudaMemset(c->ctl, 0, sizeof(Ctl));
     if ((rc = reset_ctl(c))) { mxb_ctx_destroy(c); return rc; }
@@ -788,7 +788,7 @@ int mxb_time_steps(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, double dt, int 
         cudaEventElapsedTime(&ms, e0, e1);
         *ms_stencil = ms;
     }
-    if (launches) *launches = (int64_t)nsteps * 4 * (use_demag ? 6 : 1);
+    if (launches) *launches = (int64_t)nsteps * (4 * (use_demag ? 6 : 1) + 1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return MXB_OK;

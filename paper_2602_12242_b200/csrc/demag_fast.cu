@@ -30,7 +30,7 @@ template <int L, int RMAX = 16> struct Cfg {
     static constexpr int NLc = (256 * R / L) >= 2 ? (256 * R / L) : 2;
     // fused: NK kx columns x 3 components
     static constexpr int NKraw = 256 * R / (3 * L);
-    static constexpr int NKf = L >= 512 ? 1 : (NKraw < 2 ? 2 : (NKraw > 8 ? 8 : NKraw));
+    static constexpr int NKf = NKraw < 2 ? 2 : (NKraw > 8 ? 8 : NKraw);   // >= 2: 96-byte aligned chunks
     // rows (M = L complex points per row): NR rows x 3 components
     static constexpr int NRr = (256 * R / (3 * L)) >= 1 ? (256 * R / (3 * L)) : 1;
 };
@@ -96,6 +96,34 @@ k_col_fast(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     }
 }
 
+// direct-load variant (no staging): used when the staged input would not
+// leave room for two CTAs per SM (e.g. the inverse y pass, n_in = L)
+template <int L, int DIR, int RM>
+__global__ void __launch_bounds__(Cfg<L, RM>::NLc * Cfg<L, RM>::TPL, 2)
+k_col_direct(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NL = Cfg<L, RM>::NLc;
+    extern __shared__ double2 sm[];
+    const int b = threadIdx.x % NL, t = threadIdx.x / NL;
+    const long long g = (long long)blockIdx.x * NL + b;
+    const bool ok = g < a.nlines;
+    const long long o = ok ? g / a.Q : 0, q = ok ? g - o * a.Q : 0;
+    const double2* src = a.in + o * a.OS_in + q;
+    double2 v[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        const int e = t + m * TPL;
+        v[m] = (ok && e < a.n_in) ? src[e * a.ES_in] : make_double2(0.0, 0.0);
+    }
+    fft_core<L, R, NL, true, DIR>(v, sm, b, t, tw);
+    double2* dst = a.out + o * a.OS_out + q;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int e = out_elem<L, R>(t, i);
+        if (ok && e < a.n_out) dst[e * a.ES_out] = v[i];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // fused forward * multiply * inverse along the outer axis
 // K storage: KMODE 0 complex [e*G+g][kx][6]; 2 real quarter [e'][g'][kx][6]
@@ -108,7 +136,7 @@ __device__ __forceinline__ int g_of(int r, int G) {
 }
 
 template <int L, int KMODE, int RM>
-__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, 2)
+__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, 1)
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
@@ -397,10 +425,22 @@ template <int L, int RM>
 static int col_launch(int dir, const ColArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
     constexpr int R = Cfg<L, RM>::R, NL = Cfg<L, RM>::NLc;
     const size_t sm = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n_in) * sizeof(double2);
-    if (sm > kFastSmemMax) return -1;
     const long long ntiles = (a.nlines + NL - 1) / NL;
     const int thr = NL * Cfg<L, RM>::TPL;
     int grid = 0, rc;
+    if (sm > 100 * 1024) {
+        const size_t smd = (size_t)smem_elems<L, R, NL>() * sizeof(double2);
+        if (smd > kFastSmemMax) return -1;
+        if (dir < 0) {
+            if ((rc = persistent_grid(k_col_direct<L, -1, RM>, thr, smd, 1, &grid))) return rc;
+            k_col_direct<L, -1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
+        } else {
+            if ((rc = persistent_grid(k_col_direct<L, 1, RM>, thr, smd, 1, &grid))) return rc;
+            k_col_direct<L, 1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
+        }
+        MXB_LAUNCH_CHECK();
+        return MXB_OK;
+    }
     if (dir < 0) {
         if ((rc = persistent_grid(k_col_fast<L, -1, RM>, thr, sm, ntiles, &grid))) return rc;
         k_col_fast<L, -1, RM><<<grid, thr, sm, st>>>(a, tw, halt);
@@ -487,7 +527,7 @@ int fast_cols(int dir, int L, const double2* in, double2* out, int n_in, int n_o
 #undef CASE
 }
 
-bool fast_fused_ok(int L) { return L == 1 || (pow2(L) && L <= 2048); }
+bool fast_fused_ok(int L) { return L == 1 || (pow2(L) && L <= 1024); }
 
 int fast_fused(int L, int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
                const int* halt) {

@@ -26,11 +26,18 @@
 namespace mxb {
 
 static const int kBlock = 256;
-static const int kMaxBlocks = 148 * 16;
 
 int stage_blocks(long long N) {
-    long long nb = (N + kBlock - 1) / kBlock;
-    return (int)std::min<long long>(std::max<long long>(nb, 1), kMaxBlocks);
+    const long long nb = (N + kBlock - 1) / kBlock;
+    return (int)std::max<long long>(nb, 1);
+}
+
+__global__ void k_finalize(Ctl* ctl, const double* partials, int nblk, int mode, const int* halt);
+
+int launch_finalize(const StageArgs& a, int mode, cudaStream_t st) {
+    k_finalize<<<1, 1024, 0, st>>>(a.ctl, a.partials, stage_blocks(a.g.N), mode, a.halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
 }
 
 Derived derive(const MatDev& m, const Grid& g) {
@@ -383,19 +390,6 @@ __device__ __forceinline__ void block_reduce(double v[NV], const bool is_max[NV]
     __syncthreads();
 }
 
-__device__ bool last_block_done(Ctl* ctl) {
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-        const unsigned prev = atomicInc(&ctl->arrive, total - 1);
-        last = prev == total - 1;
-    }
-    __syncthreads();
-    return last;
-}
-
 // final reduction of NV partial slots over all blocks, by the last block
 template <int NV>
 __device__ void reduce_partials(const double* partials, int nblk, const bool is_max[NV],
@@ -417,14 +411,16 @@ __device__ void reduce_partials(const double* partials, int nblk, const bool is_
 // the fused stage kernel
 // ---------------------------------------------------------------------------
 template <int MODE, bool E, bool U>
-__global__ void __launch_bounds__(256) k_stage(StageArgs a) {
+__global__ void __launch_bounds__(256, 3) k_stage(StageArgs a) {
     if (a.halt && *(volatile const int*)a.halt) return;
     const Grid& g = a.g;
     const long long N = g.N;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
     double red[4] = {0.0, 0.0, 0.0, 0.0};
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < N;
-         idx += (long long)gridDim.x * blockDim.x) {
+    // one cell per thread, blocks in cell order: the z-neighbour planes of the
+    // resident window are still in L2 when they are needed
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx < N) {
         const int i = (int)(idx % g.nx);
         const long long r = idx / g.nx;
         const int j = (int)(r % g.ny), k = (int)(r / g.ny);
@@ -434,53 +430,53 @@ __global__ void __launch_bounds__(256) k_stage(StageArgs a) {
         heff_cell<E, U>(a, a.ys, idx, i, j, k, m, cm, a.terms, h);
         if (MODE == M_HEFF) {
             a.out[idx] = h[0]; a.out[N + idx] = h[1]; a.out[2 * N + idx] = h[2];
-            continue;
-        }
-        double kk[3];
-        torque<E>(m, h, cm, a.prec, a.damp, kk);
-        if (MODE == M_RHS) {
-            a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
-            continue;
-        }
-        const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
-        double v[3];
-        if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
+        } else {
+            double kk[3];
+            torque<E>(m, h, cm, a.prec, a.damp, kk);
+            if (MODE == M_RHS) {
+                a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
+            } else {
+                const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
+                double v[3];
+                if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
 #pragma unroll
-            for (int q = 0; q < 3; ++q) v[q] = add<E>(y[q], mul<E>(a.c, kk[q]));
-            if (MODE == M_RK1) {
-                a.k1_out[idx] = kk[0]; a.k1_out[N + idx] = kk[1]; a.k1_out[2 * N + idx] = kk[2];
-            } else if (MODE == M_RK2) {
-                a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
-            } else if (MODE == M_RK3) {
+                    for (int q = 0; q < 3; ++q) v[q] = add<E>(y[q], mul<E>(a.c, kk[q]));
+                    if (MODE == M_RK1) {
+                        a.k1_out[idx] = kk[0]; a.k1_out[N + idx] = kk[1]; a.k1_out[2 * N + idx] = kk[2];
+                    } else if (MODE == M_RK2) {
+                        a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
+                    } else if (MODE == M_RK3) {
 #pragma unroll
-                for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
-            }
-        } else {  // M_RK4
+                        for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
+                    }
+                } else {  // M_RK4
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
-                v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
+                    for (int q = 0; q < 3; ++q) {
+                        const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
+                        v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
+                    }
+                }
+                if (kFinal) {
+                    if (cm.mag) {
+                        const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
+                        double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
+                        if (!(d == d) || isinf(d)) d = DBL_MAX;  // non-finite drift (llg.py:351)
+                        red[3] = d;
+                    }
+                    // a dead cell here always has drift 1 > 0.1, so the blow-up wins
+                    // (llg.py:348-355); only record it, never halt mid-kernel
+                    if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
+                    if (cm.mag) {
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+                            red[q] = E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms);
+                    }
+                } else if (a.renorm) {
+                    if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
+                }
+                a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
             }
         }
-        if (kFinal) {
-            if (cm.mag) {
-                const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
-                double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
-                if (!(d == d) || isinf(d)) d = DBL_MAX;  // non-finite drift (llg.py:351)
-                red[3] = fmax(red[3], d);
-            }
-            // a dead cell here always has drift 1 > 0.1, so the blow-up wins
-            // (llg.py:348-355); only record it, never halt mid-kernel
-            if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
-            if (cm.mag) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q)
-                    red[q] = red[q] + (E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms));
-            }
-        } else if (a.renorm) {
-            if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
-        }
-        a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
     }
     if (kFinal) {
         const bool is_max[4] = {false, false, false, true};
@@ -489,33 +485,47 @@ __global__ void __launch_bounds__(256) k_stage(StageArgs a) {
             double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
             p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = red[3];
         }
-        if (last_block_done(a.ctl)) {
-            double tot[4];
-            reduce_partials<4>(a.partials, gridDim.x, is_max, tot);
-            if (threadIdx.x == 0) {
-                Ctl* c = a.ctl;
-                const double drift = tot[3] < 0.0 ? 0.0 : tot[3];
-                if (drift == DBL_MAX || drift > 0.10) {
-                    c->drift = drift;
-                    c->halt = MXB_EBLOWUP;
-                } else if (c->halt == 0) {
-                    const double inv = (double)c->n_magnetic;
-                    double res = 0.0;
-                    for (int q = 0; q < 3; ++q) {
-                        const double mq = tot[q] / inv;
-                        res = fmax(res, fabs(mq - c->prev_mean[q]));
-                        c->mean[q] = mq;
-                        c->prev_mean[q] = mq;
-                    }
-                    c->residual = res;
-                    c->drift = drift;
-                    c->steps_done += 1;
-                    if (c->eq_tol >= 0.0 && res < c->eq_tol) c->halt = MXB_EQUILIBRATED;
-                }
-                __threadfence();
-            }
-        }
     }
+}
+
+// Deterministic final reduction of the per-block partials (fixed order for a
+// given grid) and the step bookkeeping of Simulation.run_until (llg.py:347-371):
+// blow-up test on the pre-renormalisation drift, <m>, residual, equilibrium.
+// mode 0: step, 1: mean of a field, 2: energies.
+__global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* partials, int nblk,
+                                                   int mode, const int* halt) {
+    if (halt && *(volatile const int*)halt) return;
+    const bool is_max[4] = {false, false, false, mode == 0};
+    double tot[4];
+    reduce_partials<4>(partials, nblk, is_max, tot);
+    if (threadIdx.x != 0) return;
+    Ctl* c = ctl;
+    const double inv = (double)c->n_magnetic;
+    if (mode == 1) {
+        for (int q = 0; q < 3; ++q) c->mean[q] = tot[q] / inv;
+        return;
+    }
+    if (mode == 2) {
+        for (int q = 0; q < 4; ++q) c->energies[q] = tot[q] / inv;
+        return;
+    }
+    const double drift = tot[3] < 0.0 ? 0.0 : tot[3];
+    if (drift == DBL_MAX || drift > 0.10) {
+        c->drift = drift;
+        c->halt = MXB_EBLOWUP;
+        return;
+    }
+    double res = 0.0;
+    for (int q = 0; q < 3; ++q) {
+        const double mq = tot[q] / inv;
+        res = fmax(res, fabs(mq - c->prev_mean[q]));
+        c->mean[q] = mq;
+        c->prev_mean[q] = mq;
+    }
+    c->residual = res;
+    c->drift = drift;
+    c->steps_done += 1;
+    if (c->eq_tol >= 0.0 && res < c->eq_tol) c->halt = MXB_EQUILIBRATED;
 }
 
 template <int MODE, bool E>
@@ -543,6 +553,7 @@ int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st) {
         default: set_error("bad stage mode"); return MXB_EINVAL;
     }
     MXB_LAUNCH_CHECK();
+    if (mode == M_RK4 || mode == M_EULER) return launch_finalize(a, 0, st);
     return MXB_OK;
 }
 
@@ -595,13 +606,7 @@ __global__ void k_mean(StageArgs a, const double* m) {
     block_reduce<3>(red, is_max);
     if (threadIdx.x == 0) {
         double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
-        p[0] = red[0]; p[1] = red[1]; p[2] = red[2];
-    }
-    if (last_block_done(a.ctl)) {
-        double tot[3];
-        reduce_partials<3>(a.partials, gridDim.x, is_max, tot);
-        if (threadIdx.x == 0)
-            for (int q = 0; q < 3; ++q) a.ctl->mean[q] = tot[q] / (double)a.ctl->n_magnetic;
+        p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = 0.0;
     }
 }
 
@@ -610,7 +615,9 @@ int launch_mean(const StageArgs& a, const double* m, cudaStream_t st) {
     if (a.mat.uniform) k_mean<true><<<nb, kBlock, 0, st>>>(a, m);
     else k_mean<false><<<nb, kBlock, 0, st>>>(a, m);
     MXB_LAUNCH_CHECK();
-    return MXB_OK;
+    StageArgs b = a;
+    b.halt = nullptr;
+    return launch_finalize(b, 1, st);
 }
 
 // energy densities (fields.py:200-242) summed over magnetic cells
@@ -697,12 +704,6 @@ __global__ void k_energies(StageArgs a, const double* m, const double* hd) {
         double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
         p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = red[3];
     }
-    if (last_block_done(a.ctl)) {
-        double tot[4];
-        reduce_partials<4>(a.partials, gridDim.x, is_max, tot);
-        if (threadIdx.x == 0)
-            for (int q = 0; q < 4; ++q) a.ctl->energies[q] = tot[q] / (double)a.ctl->n_magnetic;
-    }
 }
 
 int launch_energies(bool exact, const StageArgs& a, const double* m, const double* hd,
@@ -716,7 +717,9 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
         else k_energies<false, false><<<nb, kBlock, 0, st>>>(a, m, hd);
     }
     MXB_LAUNCH_CHECK();
-    return MXB_OK;
+    StageArgs b = a;
+    b.halt = nullptr;
+    return launch_finalize(b, 2, st);
 }
 
 }  // namespace mxb

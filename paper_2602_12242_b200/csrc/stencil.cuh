@@ -63,6 +63,7 @@ int launch_mean(const StageArgs& a, const double* m, cudaStream_t st);
 int launch_energies(bool exact, const StageArgs& a, const double* m, const double* hd,
                     cudaStream_t st);
 int stage_blocks(long long N);
+int launch_finalize(const StageArgs& a, int mode, cudaStream_t st);
 Derived derive(const MatDev& m, const Grid& g);
 
 }  // namespace mxb
