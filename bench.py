@@ -119,7 +119,9 @@ def demag_bytes(g, kern):
     pz, py, px = kern.padded
     hx = px // 2 + 1
     N = nx * ny * nz
-    kbytes = (48 if kern.symmetric else 96) * hx * py * pz
+    # symmetric build: parity-reduced real spectra (quarter in y and z);
+    # otherwise complex spectra over the full padded grid
+    kbytes = 48 * hx * (py // 2 + 1) * (pz // 2 + 1) if kern.symmetric else 96 * hx * py * pz
     x1 = 48 * hx * ny * nz
     x2 = 48 * hx * py * nz
     return [24 * N + x1, x1 + x2, 2 * x2 + kbytes, x2 + x1, x1 + 24 * N]
