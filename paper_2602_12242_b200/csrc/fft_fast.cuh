@@ -15,6 +15,10 @@
 
 #include "fft_generic.cuh"
 
+#ifndef MXB_TWIDDLE_PRODUCTS
+#define MXB_TWIDDLE_PRODUCTS 0
+#endif
+
 namespace mxb {
 namespace ff {
 
@@ -137,6 +141,7 @@ __device__ __forceinline__ void stages(double2 (&v)[R], double2* s, int b, int t
         for (int q = 0; q < NQ; ++q) {
             const int j = t + q * TPL;
             const int k = j & (Ns - 1);
+#if MXB_TWIDDLE_PRODUCTS
             // twiddles w^m: load the powers of two, build the rest with <= 3 products
             double2 w[r];
             w[0] = make_double2(1.0, 0.0);
@@ -147,6 +152,11 @@ __device__ __forceinline__ void stages(double2 (&v)[R], double2* s, int b, int t
                 if (m & (m - 1)) w[m] = cmul(w[m & (m - 1)], w[m & -m]);
 #pragma unroll
             for (int m = 1; m < r; ++m) v[q * r + m] = cmul(v[q * r + m], w[m]);
+#else
+            // twiddles w^m straight from the table (L1-resident): no fp64 work
+#pragma unroll
+            for (int m = 1; m < r; ++m) v[q * r + m] = cmul(v[q * r + m], twid<DIR>(tw, k * m * TS));
+#endif
             DFT<r, DIR>::run(&v[q * r]);
         }
         if constexpr (Ns * r < L) {
