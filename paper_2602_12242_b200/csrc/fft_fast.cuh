@@ -16,7 +16,7 @@
 #include "fft_generic.cuh"
 
 #ifndef MXB_TWIDDLE_PRODUCTS
-#define MXB_TWIDDLE_PRODUCTS 0
+#define MXB_TWIDDLE_PRODUCTS 1
 #endif
 
 namespace mxb {
