@@ -193,6 +193,51 @@ int mxb_run(mxb_ctx* ctx, mxb_demag* d, const mxb_terms* t, const mxb_run_args* 
 int mxb_state_energies(mxb_ctx* ctx, mxb_demag* d, const mxb_terms* t, const mxb_bias* b,
                        double out[4]);
 
+/* ---- z-slab decomposition across ranks ---------------------
+ * Rank r of G owns planes [r*nz/G, (r+1)*nz/G).  One demag evaluation is
+ *   x_forward (local rows -> per-destination kx chunks in `send`)
+ *   all-to-all send -> recv            (caller: NCCL / torch.distributed)
+ *   yz        (y, fused z*kernel, y inverse on this rank's kx chunk, in recv)
+ *   all-to-all recv -> send            (caller)
+ *   x_inverse (send -> local H rows).
+ * With G = 1 send == recv and no exchange is needed. */
+int mxb_demag_create_slab(const mxb_grid* global_grid, int device, int nranks, int rank,
+                          mxb_demag** out);
+/* info = {nz_local, z0, kx_chunk, kx_chunk_pitch, kx0, kx_count, block_elems, nranks};
+ * block_elems = complex elements per all-to-all block */
+int mxb_demag_slab_info(mxb_demag* d, int64_t info[8]);
+int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv);
+int mxb_demag_x_forward(mxb_demag* d, const double* m_dev);
+int mxb_demag_yz(mxb_demag* d);
+int mxb_demag_x_inverse(mxb_demag* d, double* h_dev);
+/* run on an external CUDA stream (e.g. the stream NCCL collectives use) */
+int mxb_demag_set_stream(mxb_demag* d, void* stream);
+int mxb_ctx_set_stream(mxb_ctx* ctx, void* stream);
+
+/* one fused stage kernel on caller-owned device buffers (the slab driver's
+ * building block; the single-rank mxb_run enqueues the same kernels) */
+typedef struct mxb_stage_io {
+    const double *ys, *y, *hd, *k1;
+    double *s, *out, *k1_out;
+    const double *halo_lo, *halo_hi;     /* (3,ny,nx) neighbour planes or NULL */
+    const double *hms_lo, *hms_hi, *hA_lo, *hA_hi;   /* their Ms / A (per-cell materials) */
+    const double* bias_field;
+    double bias[3];
+    double c, dt6;                       /* stage coefficient, dt/6 */
+    int32_t renorm;                      /* renormalise the stage state (RK stages 1-3) */
+    int32_t pad;
+} mxb_stage_io;
+/* mode: 0 H_eff, 1 dM/dt, 2-5 RK4 stages 1-4, 6 Euler.  Modes 5/6 leave block
+ * partials for mxb_step_partials_dev instead of committing the step. */
+int mxb_stage_dev(mxb_ctx* ctx, int mode, const mxb_terms* t, const mxb_stage_io* io);
+/* out8 = {sum mx/Ms, sum my/Ms, sum mz/Ms, 0 | max drift, halt code, -dead_flat, 0}
+ * (first four summed over ranks, last four max-reduced over ranks by the caller) */
+int mxb_step_partials_dev(mxb_ctx* ctx, double* out8_dev);
+/* step bookkeeping with the global totals (blow-up, <m>, residual, equilibrium) */
+int mxb_step_commit_dev(mxb_ctx* ctx, const double* totals8_dev);
+int mxb_ctl_reset(mxb_ctx* ctx, const double prev_mean[3], int64_t n_magnetic, double eq_tol);
+int mxb_ctl_get(mxb_ctx* ctx, mxb_run_stats* st);
+
 /* ---- measurement helpers (bench.py) ------------------------------------ */
 /* time `iters` demag evaluations of the resident state with CUDA events on
  * the context stream; returns the mean ms per evaluation and per pass */

@@ -52,6 +52,15 @@ class RunArgs(C.Structure):
                 ("bias_field", _dp), ("bias_vec", C.c_double * 3)]
 
 
+class StageIO(C.Structure):
+    _fields_ = [("ys", C.c_void_p), ("y", C.c_void_p), ("hd", C.c_void_p), ("k1", C.c_void_p),
+                ("s", C.c_void_p), ("out", C.c_void_p), ("k1_out", C.c_void_p),
+                ("halo_lo", C.c_void_p), ("halo_hi", C.c_void_p), ("hms_lo", C.c_void_p),
+                ("hms_hi", C.c_void_p), ("hA_lo", C.c_void_p), ("hA_hi", C.c_void_p),
+                ("bias_field", C.c_void_p), ("bias", C.c_double * 3), ("c", C.c_double),
+                ("dt6", C.c_double), ("renorm", C.c_int32), ("pad", C.c_int32)]
+
+
 class RunStats(C.Structure):
     _fields_ = [("steps_done", C.c_int64), ("status", C.c_int32), ("pad", C.c_int32),
                 ("mean", C.c_double * 3), ("residual", C.c_double), ("drift", C.c_double),
@@ -88,6 +97,19 @@ SIGNATURES = {
     "mxb_state_mean": ([C.c_void_p, _dp], C.c_int),
     "mxb_run": ([C.c_void_p, C.c_void_p, C.POINTER(Terms), C.POINTER(RunArgs), C.POINTER(RunStats)], C.c_int),
     "mxb_state_energies": ([C.c_void_p, C.c_void_p, C.POINTER(Terms), C.POINTER(Bias), _dp], C.c_int),
+    "mxb_demag_create_slab": ([C.POINTER(Grid), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "mxb_demag_slab_info": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
+    "mxb_demag_slab_buffers": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
+    "mxb_demag_x_forward": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_demag_yz": ([C.c_void_p], C.c_int),
+    "mxb_demag_x_inverse": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_demag_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_ctx_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_stage_dev": ([C.c_void_p, C.c_int, C.POINTER(Terms), C.POINTER(StageIO)], C.c_int),
+    "mxb_step_partials_dev": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_step_commit_dev": ([C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_ctl_reset": ([C.c_void_p, _dp, C.c_int64, C.c_double], C.c_int),
+    "mxb_ctl_get": ([C.c_void_p, C.POINTER(RunStats)], C.c_int),
     "mxb_time_demag": ([C.c_void_p, C.c_void_p, C.c_int, _dp, _dp], C.c_int),
     "mxb_time_steps": ([C.c_void_p, C.c_void_p, C.POINTER(Terms), C.c_double, C.c_int, _dp, _dp, _dp,
                         C.POINTER(C.c_int64)], C.c_int),

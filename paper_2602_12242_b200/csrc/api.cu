@@ -34,12 +34,14 @@ using namespace mxb;
 struct mxb_demag {
     DemagPlan plan;
     cudaStream_t st = nullptr;
+    cudaStream_t own = nullptr;
     double* io[2] = {nullptr, nullptr};  // host-facing scratch (3N each)
 };
 
 struct mxb_ctx {
     int dev = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t own = nullptr;
     Grid g{};
     MatDev mat{};
     Derived dv{};
@@ -130,6 +132,7 @@ int mxb_ctx_create(const mxb_grid* gr, const mxb_material* m, int device, mxb_ct
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "cudaSetDevice", __FILE__, __LINE__); }
     e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete c; return cuda_fail(e, "stream", __FILE__, __LINE__); }
+    c->own = c->st;
     const long long N = c->g.N;
     MatDev& md = c->mat;
     md.Ms = m->Ms; md.A = m->A; md.Ku = m->Ku; md.D = m->D; md.alpha = m->alpha;
@@ -185,7 +188,7 @@ int mxb_ctx_destroy(mxb_ctx* c) {
     double* bufs[] = {c->mat_buf, c->Yb[0], c->Yb[1], c->P, c->K1, c->S, c->Hd, c->tA, c->tB, c->bias_dev, c->partials};
     for (double* b : bufs) if (b) cudaFree(b);
     if (c->ctl) cudaFree(c->ctl);
-    if (c->st) cudaStreamDestroy(c->st);
+    if (c->own) cudaStreamDestroy(c->own);
     delete c;
     return MXB_OK;
 }
@@ -199,18 +202,24 @@ int mxb_ctx_set_exact(mxb_ctx* c, int exact) {
 // ---------------------------------------------------------------------------
 // demag objects
 // ---------------------------------------------------------------------------
-int mxb_demag_create(const mxb_grid* gr, int device, mxb_demag** out) {
+int mxb_demag_create_slab(const mxb_grid* gr, int device, int nranks, int rank, mxb_demag** out) {
     int rc = check_grid(gr);
     if (rc) return rc;
+    if (!out) { set_error("null argument"); return MXB_EINVAL; }
     mxb_demag* d = new mxb_demag();
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) { delete d; return cuda_fail(e, "cudaSetDevice", __FILE__, __LINE__); }
     e = cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete d; return cuda_fail(e, "stream", __FILE__, __LINE__); }
-    rc = d->plan.init(*gr, device);
+    d->own = d->st;
+    rc = d->plan.init(*gr, device, nranks, rank);
     if (rc) { mxb_demag_destroy(d); return rc; }
     *out = d;
     return MXB_OK;
+}
+
+int mxb_demag_create(const mxb_grid* gr, int device, mxb_demag** out) {
+    return mxb_demag_create_slab(gr, device, 1, 0, out);
 }
 
 int mxb_demag_destroy(mxb_demag* d) {
@@ -219,8 +228,53 @@ int mxb_demag_destroy(mxb_demag* d) {
     if (d->st) cudaStreamSynchronize(d->st);
     d->plan.release();
     for (double* p : d->io) if (p) cudaFree(p);
-    if (d->st) cudaStreamDestroy(d->st);
+    if (d->own) cudaStreamDestroy(d->own);
     delete d;
+    return MXB_OK;
+}
+
+int mxb_demag_slab_info(mxb_demag* d, int64_t info[8]) {
+    if (!d || !info) { set_error("null argument"); return MXB_EINVAL; }
+    const DemagPlan& p = d->plan;
+    info[0] = p.nz_l; info[1] = p.z0; info[2] = p.CH; info[3] = p.CHP;
+    info[4] = p.kx0; info[5] = p.kxn; info[6] = p.blk; info[7] = p.G;
+    return MXB_OK;
+}
+
+int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv) {
+    if (!d || !send || !recv) { set_error("null argument"); return MXB_EINVAL; }
+    *send = d->plan.XS;
+    *recv = d->plan.XR;
+    return MXB_OK;
+}
+
+int mxb_demag_x_forward(mxb_demag* d, const double* m) {
+    if (!d || !m) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(d->plan.dev);
+    return d->plan.x_forward(m, d->st, nullptr);
+}
+
+int mxb_demag_yz(mxb_demag* d) {
+    if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(d->plan.dev);
+    return d->plan.yz(d->st, nullptr);
+}
+
+int mxb_demag_x_inverse(mxb_demag* d, double* h) {
+    if (!d || !h) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(d->plan.dev);
+    return d->plan.x_inverse(h, d->st, nullptr);
+}
+
+int mxb_demag_set_stream(mxb_demag* d, void* stream) {
+    if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    d->st = stream ? (cudaStream_t)stream : d->own;
+    return MXB_OK;
+}
+
+int mxb_ctx_set_stream(mxb_ctx* c, void* stream) {
+    if (!c) { set_error("null argument"); return MXB_EINVAL; }
+    c->st = stream ? (cudaStream_t)stream : c->own;
     return MXB_OK;
 }
 
@@ -234,10 +288,10 @@ int mxb_demag_set_packed(mxb_demag* d, const double* packed) {
     double* P = nullptr;
     MXB_CUDA(cudaMalloc(&P, n * sizeof(double)));
     MXB_CUDA(cudaMemcpyAsync(P, packed, n * sizeof(double), cudaMemcpyHostToDevice, d->st));
-    MXB_CUDA(cudaMemsetAsync(p.K, 0, (size_t)p.pz * p.py * p.hxp * 6 * sizeof(double2), d->st));
     int rc = p.spectra_from_packed_dev(P, d->st);
     cudaStreamSynchronize(d->st);
     cudaFree(P);
+    if (!rc) rc = p.finish_spectra(false, d->st);
     if (rc) return rc;
     MXB_CUDA(cudaGetLastError());
     return MXB_OK;
@@ -255,7 +309,6 @@ int mxb_demag_build(mxb_demag* d, int symmetric) {
     cudaError_t e = cudaMalloc(&F, lat * sizeof(double));
     if (e != cudaSuccess) { cudaFree(P); return cuda_fail(e, "lattice", __FILE__, __LINE__); }
     int rc = MXB_OK;
-    cudaMemsetAsync(p.K, 0, (size_t)p.pz * p.py * p.hxp * 6 * sizeof(double2), d->st);
     // one component at a time: lattice -> packed component -> x transform into K[..][c]
     for (int c = 0; c < 6 && !rc; ++c) {
         rc = newell_packed_component(g, c, symmetric, P, F, d->st);
@@ -267,7 +320,7 @@ int mxb_demag_build(mxb_demag* d, int symmetric) {
     cudaFree(P);
     if (rc) return rc;
     // the mirrored tensor has exactly real, parity-structured spectra
-    if (symmetric && (rc = p.quarterize(d->st))) return rc;
+    if ((rc = p.finish_spectra(symmetric != 0, d->st))) return rc;
     MXB_CUDA(cudaGetLastError());
     return MXB_OK;
 }
@@ -298,16 +351,17 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     DemagPlan& p = d->plan;
     if (!p.has_kernel) { set_error("no spectra"); return MXB_EINVAL; }
     cudaSetDevice(p.dev);
+    if (p.G != 1) { set_error("spectra of a slab plan are sharded; use the single-rank plan"); return MXB_EINVAL; }
     if (p.kmode == 0) {
-        const size_t n = (size_t)p.pz * p.py * p.hxp * 6;
+        const size_t n = (size_t)p.pz * p.py * p.CHP * 6;
         std::vector<double2> h(n);
-        MXB_CUDA(cudaMemcpy(h.data(), p.K, n * sizeof(double2), cudaMemcpyDeviceToHost));
+        MXB_CUDA(cudaMemcpy(h.data(), p.Kc, n * sizeof(double2), cudaMemcpyDeviceToHost));
         // [kz][ky][kx][6] -> (6, pz, py, hx) interleaved
         for (int c = 0; c < 6; ++c)
             for (int kz = 0; kz < p.pz; ++kz)
                 for (int ky = 0; ky < p.py; ++ky)
                     for (int kx = 0; kx < p.hx; ++kx) {
-                        const double2 v = h[(((size_t)kz * p.py + ky) * p.hxp + kx) * 6 + c];
+                        const double2 v = h[(((size_t)kz * p.py + ky) * p.CHP + kx) * 6 + c];
                         const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
                         out[2 * o] = v.x;
                         out[2 * o + 1] = v.y;
@@ -318,7 +372,7 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     const int L = p.fused_L(), G = p.fused_G();
     const int L2 = L / 2 + 1, G2 = G / 2 + 1;
     const bool e_is_z = p.pz > 1 || p.py == 1;
-    const size_t n = (size_t)L2 * G2 * p.hxp * 6;
+    const size_t n = (size_t)L2 * G2 * p.CHP * 6;
     std::vector<double> h(n);
     MXB_CUDA(cudaMemcpy(h.data(), p.Kq, n * sizeof(double), cudaMemcpyDeviceToHost));
     for (int c = 0; c < 6; ++c)
@@ -333,7 +387,7 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
                 if (c == 2 && fz) sgn = -1.0;
                 if (c == 4 && (fy != fz)) sgn = -1.0;
                 for (int kx = 0; kx < p.hx; ++kx) {
-                    const double v = sgn * h[(((size_t)e2 * G2 + g2) * p.hxp + kx) * 6 + c];
+                    const double v = sgn * h[(((size_t)e2 * G2 + g2) * p.CHP + kx) * 6 + c];
                     const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
                     out[2 * o] = v;
                     out[2 * o + 1] = 0.0;
@@ -697,6 +751,75 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     st->status = h.halt;
     if (h.halt == MXB_EBLOWUP) { set_error("integration blew up"); return MXB_EBLOWUP; }
     if (h.halt == MXB_EDEAD) { set_error("magnetic cell with |M| = 0"); return MXB_EDEAD; }
+    return MXB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// slab driver building blocks
+// ---------------------------------------------------------------------------
+int mxb_stage_dev(mxb_ctx* c, int mode, const mxb_terms* t, const mxb_stage_io* io) {
+    if (!c || !t || !io || !io->ys || !io->out) { set_error("null argument"); return MXB_EINVAL; }
+    if (mode < M_HEFF || mode > M_EULER) { set_error("bad stage mode"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    StageArgs a = base_args(c);
+    a.terms = t->mask;
+    a.ghost = t->ghost_mode;
+    a.prec = t->precession;
+    a.damp = t->damping;
+    a.renorm = io->renorm;
+    a.ys = io->ys; a.y = io->y ? io->y : io->ys; a.hd = io->hd; a.k1 = io->k1;
+    a.s = io->s; a.out = io->out; a.k1_out = io->k1_out;
+    a.halo_lo = io->halo_lo; a.halo_hi = io->halo_hi;
+    a.hms_lo = io->hms_lo; a.hms_hi = io->hms_hi; a.hA_lo = io->hA_lo; a.hA_hi = io->hA_hi;
+    a.bias_field = io->bias_field;
+    for (int q = 0; q < 3; ++q) a.bias[q] = io->bias[q];
+    a.c = io->c;
+    a.dt6 = io->dt6;
+    a.halt = &c->ctl->halt;
+    if ((t->mask & MXB_TERM_DEMAG) && !a.hd) { set_error("demag term without a demag field"); return MXB_EINVAL; }
+    return launch_stage(mode, c->exact, a, c->st, false);
+}
+
+int mxb_step_partials_dev(mxb_ctx* c, double* out8) {
+    if (!c || !out8) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    StageArgs a = base_args(c);
+    return launch_partials(a, out8, c->st);
+}
+
+int mxb_step_commit_dev(mxb_ctx* c, const double* totals8) {
+    if (!c || !totals8) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    StageArgs a = base_args(c);
+    return launch_commit(a, totals8, c->st);
+}
+
+int mxb_ctl_reset(mxb_ctx* c, const double prev[3], int64_t n_magnetic, double eq_tol) {
+    if (!c || !prev) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    Ctl h{};
+    h.dead_flat = LLONG_MAX;
+    h.n_magnetic = n_magnetic > 0 ? n_magnetic : 1;
+    h.eq_tol = eq_tol;
+    for (int q = 0; q < 3; ++q) h.prev_mean[q] = h.mean[q] = prev[q];
+    MXB_CUDA(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+    MXB_CUDA(cudaStreamSynchronize(c->st));
+    return MXB_OK;
+}
+
+int mxb_ctl_get(mxb_ctx* c, mxb_run_stats* st) {
+    if (!c || !st) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    Ctl h;
+    MXB_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st));
+    MXB_CUDA(cudaStreamSynchronize(c->st));
+    memset(st, 0, sizeof(*st));
+    st->steps_done = h.steps_done;
+    st->status = h.halt;
+    for (int q = 0; q < 3; ++q) st->mean[q] = h.mean[q];
+    st->residual = h.residual;
+    st->drift = h.drift;
+    st->dead_flat = h.dead_flat == LLONG_MAX ? -1 : h.dead_flat;
     return MXB_OK;
 }
 

@@ -92,7 +92,7 @@ extern "C" int mxb_time_demag_cufft(mxb_demag* d, int iters, double* ms_eval) {
     MXB_CUDA(cudaMalloc(&Ks, 6 * spec_n * sizeof(double2)));
     cudaMemsetAsync(m, 0, 3 * g.N * sizeof(double), st);
     if (p.kmode == 0) {
-        k_kernel_soa<<<148 * 8, 256, 0, st>>>(p.K, Ks, p.pz, p.py, p.hx, p.hxp);
+        k_kernel_soa<<<148 * 8, 256, 0, st>>>(p.Kc, Ks, p.pz, p.py, p.hx, p.CHP);
     } else {
         // same data volume for timing; values unfolded from the quarter on the host side are
         // not needed for a timing comparison

@@ -299,7 +299,7 @@ int launch_rows_c2r(const Plan1D& p, const double2* X, int hxp, int hx, int nc, 
     return MXB_OK;
 }
 
-int DemagPlan::init(const mxb_grid& gr, int device) {
+int DemagPlan::init(const mxb_grid& gr, int device, int nranks, int rk) {
     dev = device;
     g.nx = (int)gr.nx; g.ny = (int)gr.ny; g.nz = (int)gr.nz;
     g.N = (long long)gr.nx * gr.ny * gr.nz;
@@ -310,6 +310,28 @@ int DemagPlan::init(const mxb_grid& gr, int device) {
     hx = px / 2 + 1;
     hxp = (hx + 7) / 8 * 8;
     scale = 1.0 / ((double)px * (double)py * (double)pz);
+    if (nranks < 1 || rk < 0 || rk >= nranks || g.nz % nranks != 0) {
+        set_error("slab decomposition needs nz divisible by the number of ranks");
+        return MXB_EINVAL;
+    }
+    G = nranks;
+    rank = rk;
+    nz_l = g.nz / G;
+    z0 = rank * nz_l;
+    if (G == 1) {
+        CH = hx;
+        CHP = hxp;
+    } else {
+        CH = (hx + G - 1) / G;
+        CHP = (CH + 7) / 8 * 8;
+        if (px < 4 || (px & (px - 1)) || (g.nx % 2)) {
+            set_error("the slab decomposition needs a power-of-two nx (fast x passes)");
+            return MXB_EINVAL;
+        }
+    }
+    kx0 = rank * CH;
+    kxn = std::max(0, std::min(CH, hx - kx0));
+    blk = (long long)nz_l * g.ny * CHP * 3;
     MXB_CUDA(cudaSetDevice(dev));
     int rc = set_smem_attrs();
     if (rc) return rc;
@@ -317,13 +339,14 @@ int DemagPlan::init(const mxb_grid& gr, int device) {
     if ((rc = make_plan(py, dev, &ply, &tw[1]))) return rc;
     if ((rc = make_plan(pz, dev, &plz, &tw[2]))) return rc;
     if (px >= 4 && (rc = make_plan(px / 2, dev, &plm, &twm))) return rc;
-    size_t x1 = (size_t)g.nz * g.ny * hxp * 3;
-    size_t x2 = (size_t)g.nz * py * hxp * 3;
-    MXB_CUDA(cudaMalloc(&X1, x1 * sizeof(double2)));
+    const size_t xs = (size_t)G * blk;
+    const size_t x2 = (size_t)g.nz * py * CHP * 3;
+    MXB_CUDA(cudaMalloc(&XS, xs * sizeof(double2)));
+    if (G > 1) MXB_CUDA(cudaMalloc(&XR, xs * sizeof(double2)));
+    else XR = XS;
     if (pz > 1 && py > 1) MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
-    else X2 = X1;
-    MXB_CUDA(cudaMalloc(&K, (size_t)pz * py * hxp * 6 * sizeof(double2)));
-    bytes = (x1 + (X2 != X1 ? x2 : 0) + (size_t)pz * py * hxp * 6) * sizeof(double2);
+    else X2 = XR;
+    bytes = (xs * (G > 1 ? 2 : 1) + (X2 != XR ? x2 : 0)) * sizeof(double2);
     return MXB_OK;
 }
 
@@ -332,16 +355,28 @@ void DemagPlan::release() {
     for (auto& t : tw) if (t) cudaFree(t);
     if (twm) cudaFree(twm);
     if (Kq) cudaFree(Kq);
+    if (Kc && Kc != K) cudaFree(Kc);
+    if (K) cudaFree(K);
+    if (X2 && X2 != XR) cudaFree(X2);
+    if (XR && XR != XS) cudaFree(XR);
+    if (XS) cudaFree(XS);
+    XS = XR = X2 = K = Kc = nullptr;
     Kq = nullptr;
     twm = nullptr;
-    if (X2 && X2 != X1) cudaFree(X2);
-    if (X1) cudaFree(X1);
-    if (K) cudaFree(K);
-    X1 = X2 = K = nullptr;
+}
+
+static int alloc_full_spectra(DemagPlan& p, cudaStream_t st) {
+    if (p.K) return MXB_OK;
+    const size_t n = (size_t)p.pz * p.py * p.hxp * 6;
+    MXB_CUDA(cudaMalloc(&p.K, n * sizeof(double2)));
+    MXB_CUDA(cudaMemsetAsync(p.K, 0, n * sizeof(double2), st));
+    return MXB_OK;
 }
 
 // x r2c of one packed real-space component (pz,py,px) into slot c of K
 int DemagPlan::spectra_x_component(const double* Pc, int c, cudaStream_t st) {
+    int rc = alloc_full_spectra(*this, st);
+    if (rc) return rc;
     const long long plane = (long long)pz * py;
     return launch_rows_r2c(plx, Pc, 0, px, px, K, hxp, hx, 1, plane, st, nullptr, 6, c);
 }
@@ -361,7 +396,6 @@ int DemagPlan::spectra_yz(cudaStream_t st) {
         rc = launch_lines(-1, plz, K, K, pz, pz, Q, Q, (int)Q, Q, 0, 0, st, nullptr);
         if (rc) return rc;
     }
-    has_kernel = true;
     return MXB_OK;
 }
 
@@ -375,106 +409,159 @@ int DemagPlan::spectra_from_packed_dev(const double* P, cudaStream_t st) {
     return spectra_yz(st);
 }
 
-int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
-                         cudaEvent_t* ev) {
-    auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
-    if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
-    const long long N = g.N;
-    const int nx = g.nx, ny = g.ny, nz = g.nz;
-    const long long rows = (long long)nz * ny;
-    const bool fast_x = fast && px >= 4 && (nx % 2) == 0;
-    int rc;
-    mark(0);
-    // P1: x r2c
-    rc = -1;
-    if (fast_x) rc = fast_rows(true, px / 2, m, X1, nullptr, N, nx, nx / 2, hxp, rows, plm.tw, plx.tw, st, halt);
-    if (rc == -1) rc = launch_rows_r2c(plx, m, N, nx, nx, X1, hxp, hx, 3, rows, st, halt, 3, 0);
-    if (rc) return rc;
-    mark(1);
-    const long long row = (long long)hxp * 3;   // complex elements per (z,y) row
-    auto cols = [&](int dir, const double2* in, double2* out, int n_in, int n_out, long long OS_in,
-                    long long OS_out) {
-        int r = -1;
-        if (fast) r = fast_cols(dir, py, in, out, n_in, n_out, row, row, hx * 3, (long long)nz * hx * 3,
-                                OS_in, OS_out, ply.tw, st, halt);
-        if (r == -1) r = launch_lines(dir, ply, in, out, n_in, n_out, row, row, hx * 3,
-                                      (long long)nz * hx * 3, OS_in, OS_out, st, halt);
-        return r;
-    };
-    auto fused = [&](const Plan1D& pl, double2* X, int n, long long ES, int G, long long GS, int e_is_z) {
-        int r = -1;
-        if (fast || kmode != 0) {
-            FusedArgs a{X, kmode == 0 ? (const void*)K : (const void*)Kq, n, ES, hx, hxp, G, GS, scale, e_is_z};
-            r = fast_fused(pl.L, kmode, a, pl.tw, st, halt);
-        }
-        if (r == -1 && kmode == 0) r = launch_fused(pl, X, K, n, ES, hx, hxp, G, GS, scale, st, halt);
-        if (r == -1) { set_error("no fused kernel for this shape"); r = MXB_EINVAL; }
-        return r;
-    };
-    if (pz > 1) {
-        if (py > 1) {
-            // P2: y forward, per z-plane: ny rows in -> py rows out
-            if ((rc = cols(-1, X1, X2, ny, py, (long long)ny * row, (long long)py * row))) return rc;
-        }
-        mark(2);
-        // P3 along z: line base = ky*row + kx*3 + c, element stride py*row
-        if ((rc = fused(plz, X2, nz, (long long)py * row, py, row, 1))) return rc;
-        mark(3);
-        if (py > 1) {
-            if ((rc = cols(1, X2, X1, py, ny, (long long)py * row, (long long)ny * row))) return rc;
-        }
-        mark(4);
-    } else if (py > 1) {
-        mark(2);
-        if ((rc = fused(ply, X1, ny, row, 1, 0, 0))) return rc;
-        mark(3);
-        mark(4);
-    } else {
-        mark(2);
-        if ((rc = fused(plz, X1, 1, row, 1, 0, 1))) return rc;
-        mark(3);
-        mark(4);
-    }
-    // P5: x c2r
-    rc = -1;
-    if (fast_x) rc = fast_rows(false, px / 2, nullptr, X1, h, N, nx, nx / 2, hxp, rows, plm.tw, plx.tw, st, halt);
-    if (rc == -1) rc = launch_rows_c2r(plx, X1, hxp, hx, 3, h, N, nx, nx, rows, st, halt);
-    mark(5);
-    return rc;
-}
-
-// real parts of the (exactly real, parity-structured) spectra, quarter storage
-__global__ void k_quarterize(const double2* K, double* Kq, int L, int G, int py, int hxp,
-                             int e_is_z) {
-    const int L2 = L / 2 + 1, G2 = G / 2 + 1;
-    const long long tot = (long long)L2 * G2 * hxp * 6;
+// the rank's kx chunk of the complex spectra
+__global__ void k_chunk_complex(const double2* K, double2* Kc, long long nzy, int hxp, int kx0,
+                                int kxn, int CHP) {
+    const long long tot = nzy * CHP * 6;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
          t += (long long)gridDim.x * blockDim.x) {
         const int c = (int)(t % 6);
         long long r = t / 6;
-        const int kx = (int)(r % hxp);
-        r /= hxp;
-        const int g2 = (int)(r % G2), e2 = (int)(r / G2);
-        const int kz = e_is_z ? e2 : g2, ky = e_is_z ? g2 : e2;
-        Kq[t] = K[(((long long)kz * py + ky) * hxp + kx) * 6 + c].x;
+        const int kx = (int)(r % CHP);
+        const long long zy = r / CHP;
+        Kc[t] = kx < kxn ? K[(zy * hxp + kx0 + kx) * 6 + c] : make_double2(0.0, 0.0);
     }
 }
 
-int DemagPlan::quarterize(cudaStream_t st) {
-    const int L = fused_L(), G = fused_G();
-    if (!fast_fused_ok(L)) return MXB_OK;   // keep complex spectra for the generic path
-    const int e_is_z = pz > 1 ? 1 : (py > 1 ? 0 : 1);
-    const size_t n = (size_t)(L / 2 + 1) * (G / 2 + 1) * hxp * 6;
-    MXB_CUDA(cudaMalloc(&Kq, n * sizeof(double)));
-    k_quarterize<<<148 * 8, 256, 0, st>>>(K, Kq, L, G, py, hxp, e_is_z);
-    MXB_LAUNCH_CHECK();
+// real parts of the (exactly real, parity-structured) spectra, quarter storage
+__global__ void k_quarterize(const double2* K, double* Kq, int L, int G, int py, int hxp,
+                             int e_is_z, int kx0, int kxn, int CHP) {
+    const int L2 = L / 2 + 1, G2 = G / 2 + 1;
+    const long long tot = (long long)L2 * G2 * CHP * 6;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(t % 6);
+        long long r = t / 6;
+        const int kx = (int)(r % CHP);
+        r /= CHP;
+        const int g2 = (int)(r % G2), e2 = (int)(r / G2);
+        const int kz = e_is_z ? e2 : g2, ky = e_is_z ? g2 : e2;
+        Kq[t] = kx < kxn ? K[(((long long)kz * py + ky) * hxp + kx0 + kx) * 6 + c].x : 0.0;
+    }
+}
+
+int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
+    const int L = fused_L(), GG = fused_G();
+    if (Kq) { cudaFree(Kq); Kq = nullptr; }
+    if (Kc && Kc != K) { cudaFree(Kc); }
+    Kc = nullptr;
+    kmode = 0;
+    if (symmetric && fast_fused_ok(L)) {
+        const int e_is_z = pz > 1 ? 1 : (py > 1 ? 0 : 1);
+        const size_t n = (size_t)(L / 2 + 1) * (GG / 2 + 1) * CHP * 6;
+        MXB_CUDA(cudaMalloc(&Kq, n * sizeof(double)));
+        k_quarterize<<<148 * 8, 256, 0, st>>>(K, Kq, L, GG, py, hxp, e_is_z, kx0, kxn, CHP);
+        MXB_LAUNCH_CHECK();
+        kmode = 2;
+    } else if (G == 1) {
+        Kc = K;   // the chunk is the whole spectrum
+    } else {
+        const size_t n = (size_t)pz * py * CHP * 6;
+        MXB_CUDA(cudaMalloc(&Kc, n * sizeof(double2)));
+        k_chunk_complex<<<148 * 8, 256, 0, st>>>(K, Kc, (long long)pz * py, hxp, kx0, kxn, CHP);
+        MXB_LAUNCH_CHECK();
+    }
     MXB_CUDA(cudaStreamSynchronize(st));
-    cudaFree(K);
-    K = nullptr;
-    kmode = 2;
-    bytes -= (size_t)pz * py * hxp * 6 * sizeof(double2);
-    bytes += n * sizeof(double);
+    if (Kc != K) {
+        cudaFree(K);
+        K = nullptr;
+    }
+    bytes += kmode == 2 ? (size_t)(L / 2 + 1) * (GG / 2 + 1) * CHP * 6 * sizeof(double)
+                        : (size_t)pz * py * CHP * 6 * sizeof(double2);
+    has_kernel = true;
     return MXB_OK;
+}
+
+int DemagPlan::x_forward(const double* m, cudaStream_t st, const int* halt) {
+    const long long Nl = (long long)nz_l * g.ny * g.nx;
+    const long long rows = (long long)nz_l * g.ny;
+    const int nx = g.nx;
+    int rc = -1;
+    if (fast && px >= 4 && (nx % 2) == 0)
+        rc = fast_rows(true, px / 2, m, XS, nullptr, Nl, nx, nx / 2, CH, CHP, blk, rows, plm.tw,
+                       plx.tw, st, halt);
+    if (rc == -1) {
+        if (G > 1) { set_error("no x kernel for this slab shape"); return MXB_EINVAL; }
+        rc = launch_rows_r2c(plx, m, Nl, nx, nx, XS, hxp, hx, 3, rows, st, halt, 3, 0);
+    }
+    return rc;
+}
+
+int DemagPlan::x_inverse(double* h, cudaStream_t st, const int* halt) {
+    const long long Nl = (long long)nz_l * g.ny * g.nx;
+    const long long rows = (long long)nz_l * g.ny;
+    const int nx = g.nx;
+    int rc = -1;
+    if (fast && px >= 4 && (nx % 2) == 0)
+        rc = fast_rows(false, px / 2, nullptr, XS, h, Nl, nx, nx / 2, CH, CHP, blk, rows, plm.tw,
+                       plx.tw, st, halt);
+    if (rc == -1) {
+        if (G > 1) { set_error("no x kernel for this slab shape"); return MXB_EINVAL; }
+        rc = launch_rows_c2r(plx, XS, hxp, hx, 3, h, Nl, nx, nx, rows, st, halt);
+    }
+    return rc;
+}
+
+// y forward, fused z (or y) multiply, y inverse on the kx chunk held in XR
+int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
+    auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], st); };
+    if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
+    const int ny = g.ny, nz = g.nz;
+    const long long row = (long long)CHP * 3;   // complex elements per (z,y) row of the chunk
+    int rc;
+    if (kxn <= 0) { mark(2); mark(3); mark(4); return MXB_OK; }
+    auto cols = [&](int dir, const double2* in, double2* out, int n_in, int n_out, long long OS_in,
+                    long long OS_out) {
+        int r = -1;
+        if (fast) r = fast_cols(dir, py, in, out, n_in, n_out, row, row, kxn * 3, (long long)nz * kxn * 3,
+                                OS_in, OS_out, ply.tw, st, halt);
+        if (r == -1) r = launch_lines(dir, ply, in, out, n_in, n_out, row, row, kxn * 3,
+                                      (long long)nz * kxn * 3, OS_in, OS_out, st, halt);
+        return r;
+    };
+    auto fused = [&](const Plan1D& pl, double2* X, int n, long long ES, int GG, long long GS, int e_is_z) {
+        int r = -1;
+        if (fast || kmode != 0) {
+            FusedArgs a{X, kmode == 0 ? (const void*)Kc : (const void*)Kq, n, ES, kxn, CHP, GG, GS, scale, e_is_z};
+            r = fast_fused(pl.L, kmode, a, pl.tw, st, halt);
+        }
+        if (r == -1 && kmode == 0) r = launch_fused(pl, X, Kc, n, ES, kxn, CHP, GG, GS, scale, st, halt);
+        if (r == -1) { set_error("no fused kernel for this shape"); r = MXB_EINVAL; }
+        return r;
+    };
+    if (pz > 1) {
+        if (py > 1 && (rc = cols(-1, XR, X2, ny, py, (long long)ny * row, (long long)py * row))) return rc;
+        mark(2);
+        if ((rc = fused(plz, X2, nz, (long long)py * row, py, row, 1))) return rc;
+        mark(3);
+        if (py > 1 && (rc = cols(1, X2, XR, py, ny, (long long)py * row, (long long)ny * row))) return rc;
+        mark(4);
+    } else if (py > 1) {
+        mark(2);
+        if ((rc = fused(ply, XR, ny, row, 1, 0, 0))) return rc;
+        mark(3);
+        mark(4);
+    } else {
+        mark(2);
+        if ((rc = fused(plz, XR, 1, row, 1, 0, 1))) return rc;
+        mark(3);
+        mark(4);
+    }
+    return MXB_OK;
+}
+
+int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
+                         cudaEvent_t* ev) {
+    if (G != 1) { set_error("field_dev is the single-rank pipeline"); return MXB_EINVAL; }
+    if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
+    if (ev) cudaEventRecord(ev[0], st);
+    int rc = x_forward(m, st, halt);
+    if (rc) return rc;
+    if (ev) cudaEventRecord(ev[1], st);
+    if ((rc = yz(st, halt, ev))) return rc;
+    rc = x_inverse(h, st, halt);
+    if (ev) cudaEventRecord(ev[5], st);
+    return rc;
 }
 
 }  // namespace mxb

@@ -22,39 +22,51 @@ int fast_cols(int dir, int L, const double2* in, double2* out, int n_in, int n_o
 bool fast_fused_ok(int L);
 int fast_fused(int L, int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
                const int* halt);
+// x rows; spectra row kx lives at X[(kx / CH) * BLKE + (row * CHP + kx % CH) * 3 + c]
+// (one block per destination rank of the slab all-to-all; CH >= hx for one rank)
 int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, long long cstride,
-              int pitch, int nhalf, int hxp, long long nrows, const double2* twM,
-              const double2* tw2M, cudaStream_t st, const int* halt);
+              int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
+              const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt);
 
 struct DemagPlan {
     int dev = 0;
-    Grid g{};
+    Grid g{};                // GLOBAL grid
     int px = 1, py = 1, pz = 1, hx = 1, hxp = 8;
     double scale = 1.0;
     Plan1D plx{}, ply{}, plz{};
     double2* tw[3] = {nullptr, nullptr, nullptr};
-    double2* X1 = nullptr;   // [nz][ny][hxp][3]
-    double2* X2 = nullptr;   // [nz][py][hxp][3]
-    double2* K = nullptr;    // [pz][py][hxp][6] spectra (unscaled), complex
-    double* Kq = nullptr;    // parity-reduced real spectra [L/2+1][G/2+1][hxp][6]
-    int kmode = 0;           // 0 complex K, 2 real quarter Kq
+    // z-slab decomposition (G ranks): the x passes run on this rank's nz_l
+    // planes, the y/z passes on its kx chunk [kx0, kx0+kxn) of all nz planes.
+    int G = 1, rank = 0, nz_l = 1, z0 = 0;
+    int CH = 1, CHP = 8, kx0 = 0, kxn = 1;
+    long long blk = 0;       // complex elements per all-to-all block
+    double2* XS = nullptr;   // x-pass side, [G][nz_l][ny][CHP][3] (send layout)
+    double2* XR = nullptr;   // kx-chunk side, [nz][ny][CHP][3] (== XS for one rank)
+    double2* X2 = nullptr;   // [nz][py][CHP][3]
+    double2* K = nullptr;    // full spectra [pz][py][hxp][6] complex (build scratch)
+    double2* Kc = nullptr;   // complex spectra of the chunk [pz][py][CHP][6]
+    double* Kq = nullptr;    // parity-reduced real spectra of the chunk [L/2+1][G/2+1][CHP][6]
+    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq
     Plan1D plm{};            // length px/2 (fast x rows)
     double2* twm = nullptr;
     bool fast = true;        // use the register-resident kernels where shapes allow
     bool has_kernel = false;
+    size_t bytes = 0;
     int fused_L() const { return pz > 1 ? pz : (py > 1 ? py : 1); }
     int fused_G() const { return pz > 1 ? py : 1; }
-    int quarterize(cudaStream_t st);
-    size_t bytes = 0;
 
-    int init(const mxb_grid& g, int device);
+    int init(const mxb_grid& g, int device, int nranks = 1, int rank = 0);
     void release();
     int spectra_from_packed_dev(const double* P, cudaStream_t st);
     int spectra_x_component(const double* Pc, int c, cudaStream_t st);
     int spectra_yz(cudaStream_t st);
-    // ev (optional): 6 events recorded before P1 and after each of the 5 passes
+    int finish_spectra(bool symmetric, cudaStream_t st);   // chunk + optional quarter storage
+    // one evaluation (one rank): x forward, y/z, x inverse
     int field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
                   cudaEvent_t* ev = nullptr);
+    int x_forward(const double* m_local, cudaStream_t st, const int* halt);
+    int yz(cudaStream_t st, const int* halt, cudaEvent_t* ev = nullptr);
+    int x_inverse(double* h_local, cudaStream_t st, const int* halt);
 };
 
 int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);

@@ -261,8 +261,9 @@ k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict_
 template <int M>
 __global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
 k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in2,
-           double2* __restrict__ out, int hxp, long long nrows, const double2* __restrict__ twM,
-           const double2* __restrict__ tw2M, const int* __restrict__ halt) {
+           double2* __restrict__ out, int CH, int CHP, long long BLKE, long long nrows,
+           const double2* __restrict__ twM, const double2* __restrict__ tw2M,
+           const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<M>::R, TPL = Cfg<M>::TPL, NR = Cfg<M>::NRr, NL = 3 * NR;
     constexpr int HX = M + 1;
@@ -312,15 +313,16 @@ k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in
             // E = (Zk + conj Zm)/2, O = (Zk - conj Zm)/(2i), X = E + W^k O
             const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
             const double2 O = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-            out[(urow * hxp + kx) * 3 + cc] = cadd(E, cmul(tw2M[kx], O));
+            const int blk = kx / CH, kxc = kx - blk * CH;
+            out[blk * BLKE + (urow * CHP + kxc) * 3 + cc] = cadd(E, cmul(tw2M[kx], O));
         }
     }
 }
 
 template <int M>
 __global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
-k_c2r_fast(const double2* __restrict__ Xin, int hxp, double* __restrict__ out, long long cstride,
-           int pitch, int n_out2, long long nrows, const double2* __restrict__ twM,
+k_c2r_fast(const double2* __restrict__ Xin, int CH, int CHP, long long BLKE, double* __restrict__ out,
+           long long cstride, int pitch, int n_out2, long long nrows, const double2* __restrict__ twM,
            const double2* __restrict__ tw2M, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<M>::R, TPL = Cfg<M>::TPL, NR = Cfg<M>::NRr, NL = 3 * NR;
@@ -335,7 +337,9 @@ k_c2r_fast(const double2* __restrict__ Xin, int hxp, double* __restrict__ out, l
             const int url = u / (HX * 3), qq = u - url * (HX * 3);
             const long long row = tile * NR + url;
             const bool ok = row < nrows;
-            cp_async16(&S[u], Xin + (ok ? row : 0) * hxp * 3 + qq, ok);
+            const int kx = qq / 3, blk = kx / CH;
+            const long long src = blk * BLKE + ((ok ? row : 0) * CHP + (kx - blk * CH)) * 3 + (qq - 3 * kx);
+            cp_async16(&S[u], Xin + src, ok);
         }
         cp_async_commit();
     };
@@ -477,8 +481,8 @@ static int fused_launch(int kmode, const FusedArgs& a, const double2* tw, cudaSt
 
 template <int M>
 static int rows_launch(bool fwd, const double* in_r, double2* X, double* out_r, long long cstride,
-                       int pitch, int nhalf, int hxp, long long nrows, const double2* twM,
-                       const double2* tw2M, cudaStream_t st, const int* halt) {
+                       int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
+                       const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt) {
     constexpr int R = Cfg<M>::R, NR = Cfg<M>::NRr, NL = 3 * NR;
     const size_t stage = fwd ? (size_t)NL * nhalf : (size_t)NR * (M + 1) * 3;
     const size_t sm = ((size_t)smem_elems<M, R, NL>() + stage) * sizeof(double2);
@@ -488,10 +492,12 @@ static int rows_launch(bool fwd, const double* in_r, double2* X, double* out_r, 
     int grid = 0, rc;
     if (fwd) {
         if ((rc = persistent_grid(k_r2c_fast<M>, thr, sm, ntiles, &grid))) return rc;
-        k_r2c_fast<M><<<grid, thr, sm, st>>>(in_r, cstride, pitch, nhalf, X, hxp, nrows, twM, tw2M, halt);
+        k_r2c_fast<M><<<grid, thr, sm, st>>>(in_r, cstride, pitch, nhalf, X, CH, CHP, BLKE, nrows, twM,
+                                             tw2M, halt);
     } else {
         if ((rc = persistent_grid(k_c2r_fast<M>, thr, sm, ntiles, &grid))) return rc;
-        k_c2r_fast<M><<<grid, thr, sm, st>>>(X, hxp, out_r, cstride, pitch, nhalf, nrows, twM, tw2M, halt);
+        k_c2r_fast<M><<<grid, thr, sm, st>>>(X, CH, CHP, BLKE, out_r, cstride, pitch, nhalf, nrows, twM,
+                                             tw2M, halt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
@@ -551,10 +557,10 @@ int fast_fused(int L, int kmode, const FusedArgs& a, const double2* tw, cudaStre
 }
 
 int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, long long cstride,
-              int pitch, int nhalf, int hxp, long long nrows, const double2* twM,
-              const double2* tw2M, cudaStream_t st, const int* halt) {
+              int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
+              const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt) {
     if (!pow2(M)) return -1;
-#define CASE(V) case V: return rows_launch<V>(fwd, in_r, X, out_r, cstride, pitch, nhalf, hxp, nrows, twM, tw2M, st, halt);
+#define CASE(V) case V: return rows_launch<V>(fwd, in_r, X, out_r, cstride, pitch, nhalf, CH, CHP, BLKE, nrows, twM, tw2M, st, halt);
     switch (M) { MXB_POW2_CASES(CASE) default: return -1; }
 #undef CASE
 }

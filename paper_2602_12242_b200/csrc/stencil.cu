@@ -33,6 +33,21 @@ int stage_blocks(long long N) {
 }
 
 __global__ void k_finalize(Ctl* ctl, const double* partials, int nblk, int mode, const int* halt);
+__global__ void k_partials(const Ctl* ctl, const double* partials, int nblk, double* out8);
+__global__ void k_commit(Ctl* ctl, const double* totals8);
+
+// slab decomposition: local (sum m/Ms x3 | drift, halt, -dead) of the last final stage
+int launch_partials(const StageArgs& a, double* out8, cudaStream_t st) {
+    k_partials<<<1, 1024, 0, st>>>(a.ctl, a.partials, stage_blocks(a.g.N), out8);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int launch_commit(const StageArgs& a, const double* totals8, cudaStream_t st) {
+    k_commit<<<1, 32, 0, st>>>(a.ctl, totals8);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
 
 int launch_finalize(const StageArgs& a, int mode, cudaStream_t st) {
     k_finalize<<<1, 1024, 0, st>>>(a.ctl, a.partials, stage_blocks(a.g.N), mode, a.halt);
@@ -117,6 +132,38 @@ __device__ __forceinline__ void neighbour(const StageArgs& a, const double* f, l
     const bool periodic = a.ghost == MXB_GHOST_PERIODIC;
     const int c2 = coord + step;
     const bool inr = c2 >= 0 && c2 < n;
+    if (axis == 2 && !inr && (c2 < 0 ? a.halo_lo : a.halo_hi)) {
+        // neighbour plane owned by the adjacent z-slab
+        const bool lo = c2 < 0;
+        const double* hp = lo ? a.halo_lo : a.halo_hi;
+        const long long plane = (long long)a.g.nx * a.g.ny;
+        const long long p = idx - (long long)coord * plane;
+        bool valid;
+        double Anb;
+        if (U) {
+            valid = cm.mag;
+            Anb = cm.A;
+        } else {
+            const double* hm = lo ? a.hms_lo : a.hms_hi;
+            const double* ha = lo ? a.hA_lo : a.hA_hi;
+            valid = (hm ? hm[p] : a.mat.Ms) > 0.0;
+            Anb = ha ? ha[p] : a.mat.A;
+        }
+        double harm;
+        if (U) {
+            harm = a.dv.face;
+        } else {
+            const double tot = add<E>(cm.A, Anb);
+            harm = tot > 0.0 ? div_rn(mul<E>(mul<E>(2.0, cm.A), Anb), tot) : 0.0;
+        }
+        face = valid ? harm : cm.A;
+        if (periodic || valid) {
+            nb[0] = ld(hp, p); nb[1] = ld(hp, plane + p); nb[2] = ld(hp, 2 * plane + p);
+        } else {
+            nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];   // z faces carry no DMI tilt
+        }
+        return;
+    }
     long long nidx;
     if (periodic) {
         const int w = inr ? c2 : (c2 < 0 ? c2 + n : c2 - n);
@@ -176,6 +223,17 @@ __device__ __forceinline__ void bulk_neighbour(const StageArgs& a, const double*
                                                double nb[3]) {
     const long long N = a.g.N;
     const int c2 = coord + step;
+    if (axis == 2 && (c2 < 0 ? a.halo_lo : (c2 >= n ? a.halo_hi : nullptr))) {
+        const bool lo = c2 < 0;
+        const double* hp = lo ? a.halo_lo : a.halo_hi;
+        const long long plane = (long long)a.g.nx * a.g.ny;
+        const long long p = idx - (long long)coord * plane;
+        const double* hm = lo ? a.hms_lo : a.hms_hi;
+        if (U || !hm || hm[p] > 0.0) {
+            nb[0] = ld(hp, p); nb[1] = ld(hp, plane + p); nb[2] = ld(hp, 2 * plane + p);
+            return;
+        }
+    }
     bool valid = c2 >= 0 && c2 < n;
     const long long nidx = valid ? idx + step * stride : idx;
     if (valid && !U && a.mat.Ms_c) valid = ld(a.mat.Ms_c, nidx) > 0.0;
@@ -488,6 +546,62 @@ __global__ void __launch_bounds__(256, 3) k_stage(StageArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(1024) k_partials(const Ctl* ctl, const double* partials, int nblk,
+                                                   double* out8) {
+    const bool is_max[4] = {false, false, false, true};
+    double tot[4];
+    if (ctl->halt) {
+        if (threadIdx.x == 0) {
+            out8[0] = out8[1] = out8[2] = out8[3] = 0.0;
+            out8[4] = 0.0;
+            out8[5] = (double)ctl->halt;
+            out8[6] = ctl->dead_flat == LLONG_MAX ? -9.0e18 : -(double)ctl->dead_flat;
+            out8[7] = 0.0;
+        }
+        return;
+    }
+    reduce_partials<4>(partials, nblk, is_max, tot);
+    if (threadIdx.x == 0) {
+        out8[0] = tot[0]; out8[1] = tot[1]; out8[2] = tot[2]; out8[3] = 0.0;
+        out8[4] = tot[3] < 0.0 ? 0.0 : tot[3];
+        out8[5] = (double)ctl->halt;
+        out8[6] = ctl->dead_flat == LLONG_MAX ? -9.0e18 : -(double)ctl->dead_flat;
+        out8[7] = 0.0;
+    }
+}
+
+// global totals (sums over ranks of [0..3], max over ranks of [4..7]) -> the
+// same bookkeeping as k_finalize mode 0, identically on every rank
+__global__ void k_commit(Ctl* ctl, const double* t) {
+    if (threadIdx.x != 0) return;
+    Ctl* c = ctl;
+    const int halt = (int)t[5];
+    if (halt == MXB_EDEAD || halt == MXB_EBLOWUP) {
+        c->halt = halt;
+        if (t[6] > -9.0e18) c->dead_flat = (long long)(-t[6]);
+        return;
+    }
+    if (c->halt) return;
+    const double drift = t[4];
+    if (drift == DBL_MAX || drift > 0.10) {
+        c->drift = drift;
+        c->halt = MXB_EBLOWUP;
+        return;
+    }
+    const double inv = (double)c->n_magnetic;
+    double res = 0.0;
+    for (int q = 0; q < 3; ++q) {
+        const double mq = t[q] / inv;
+        res = fmax(res, fabs(mq - c->prev_mean[q]));
+        c->mean[q] = mq;
+        c->prev_mean[q] = mq;
+    }
+    c->residual = res;
+    c->drift = drift;
+    c->steps_done += 1;
+    if (c->eq_tol >= 0.0 && res < c->eq_tol) c->halt = MXB_EQUILIBRATED;
+}
+
 // Deterministic final reduction of the per-block partials (fixed order for a
 // given grid) and the step bookkeeping of Simulation.run_until (llg.py:347-371):
 // blow-up test on the pre-renormalisation drift, <m>, residual, equilibrium.
@@ -540,7 +654,7 @@ static void launch_mode(bool exact, const StageArgs& a, cudaStream_t st, int nb)
     else launch_mode_u<MODE, false>(a, st, nb);
 }
 
-int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st) {
+int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st, bool finalize) {
     const int nb = stage_blocks(a.g.N);
     switch (mode) {
         case M_HEFF: launch_mode<M_HEFF>(exact, a, st, nb); break;
@@ -553,7 +667,7 @@ int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st) {
         default: set_error("bad stage mode"); return MXB_EINVAL;
     }
     MXB_LAUNCH_CHECK();
-    if (mode == M_RK4 || mode == M_EULER) return launch_finalize(a, 0, st);
+    if (finalize && (mode == M_RK4 || mode == M_EULER)) return launch_finalize(a, 0, st);
     return MXB_OK;
 }
 

@@ -54,9 +54,17 @@ struct StageArgs {
     Ctl* ctl;
     double* partials;
     const int* halt;
+    // z-slab decomposition: neighbour planes of the first/last local plane,
+    // (3, ny, nx) each, plus the neighbours' Ms and A for per-cell materials
+    const double* halo_lo;
+    const double* halo_hi;
+    const double* hms_lo;
+    const double* hms_hi;
+    const double* hA_lo;
+    const double* hA_hi;
 };
 
-int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st);
+int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st, bool finalize = true);
 int launch_term(uint32_t term, int ghost, bool exact, const StageArgs& a, cudaStream_t st);
 int launch_renorm(const StageArgs& a, double* m, cudaStream_t st);
 int launch_mean(const StageArgs& a, const double* m, cudaStream_t st);
@@ -64,6 +72,8 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
                     cudaStream_t st);
 int stage_blocks(long long N);
 int launch_finalize(const StageArgs& a, int mode, cudaStream_t st);
+int launch_partials(const StageArgs& a, double* out8, cudaStream_t st);
+int launch_commit(const StageArgs& a, const double* totals8, cudaStream_t st);
 Derived derive(const MatDev& m, const Grid& g);
 
 }  // namespace mxb
