@@ -162,7 +162,9 @@ class CudaSlabBackend:
         self.mat = mat_local
         self.ctx = mat_local._ctx()
         self.d = demag_handle
-        self.stream = torch.cuda.current_stream(self.dev).cuda_stream
+        # torch's legacy default stream has handle 0; pass cudaStreamLegacy (0x1)
+        # so our kernels are ordered with torch's copies and collectives
+        self.stream = torch.cuda.current_stream(self.dev).cuda_stream or 1
         lib = L.load()
         L.check(lib.mxb_ctx_set_stream(self.ctx.h, C.c_void_p(self.stream)))
         shape = (3, plan.nz_local, plan.ny, plan.nx)
