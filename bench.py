@@ -14,9 +14,9 @@ larger than the 126 MB L2, so no explicit flush is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512] [--impl reference]
 
-Under torchrun (N>1) every rank runs its own replica of the workload (the
-z-slab decomposition is not wired into the bench yet); the step time is the
-max over ranks.
+Under torchrun (N>1) the 512^3 problem is z-slab decomposed over the ranks
+(strong scaling; NCCL halos, slab-FFT all-to-alls and step all-reduces); the
+step time is the max over ranks of CUDA-event timings.
 """
 from __future__ import annotations
 
@@ -149,6 +149,86 @@ def cpu_reference(n: int, steps: int, warmup: int):
     return n ** 3 * steps / el, el, cores
 
 
+def run_slab(args, rank, world, local):
+    """N > 1: the 512^3 problem z-slab decomposed over the ranks (strong scaling):
+    halo planes by send/recv, slab FFT transposes by all-to-all, step reductions
+    by all-reduce (paper_2602_12242_b200.slab)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_12242_b200 as mx
+    from paper_2602_12242_b200 import _lib as L
+    from paper_2602_12242_b200.llg import _ORDER
+    from paper_2602_12242_b200.slab import Comm, CudaSlabBackend, SlabPlan, SlabSimulation
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    mx.set_device(dev)
+    dist.init_process_group(args.backend)
+    n = args.n
+    plan = SlabPlan(n, n, n, world, rank)
+    cell = (4e-9, 4e-9, 4e-9)
+    gl = mx.GridSpec(n, n, plan.nz_local, *cell)
+    mat_l = mx.MaterialMap(gl, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
+    h = C.c_void_p()
+    t0 = time.perf_counter()
+    L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(n, n, n, *cell)._c()), dev, world,
+                                           rank, C.byref(h)))
+    L.check(L.load().mxb_demag_build(h, 1))
+    t_build = time.perf_counter() - t0
+    b = CudaSlabBackend(plan, gl, mat_l, h, dev)
+    bias = np.array([1e4, 0.0, 0.0])
+    rhs = mx.PartitionedRHS(mat_l, exchange=True, anisotropy=True, dmi=True, bias=bias)
+    mask = L.TERM_DEMAG
+    for t in rhs.enabled_terms():
+        mask |= {"exchange": L.TERM_EXCHANGE, "anisotropy": L.TERM_ANISOTROPY, "dmi": L.TERM_DMI,
+                 "bias": L.TERM_BIAS}[t]
+    terms = L.Terms(mask, L.GHOST["dmi"], 1, 1)
+    rng = np.random.default_rng(1000 + rank)      # per-slab synthetic state
+    m = mx.VectorField3(gl, rng.standard_normal(size=(3,) + gl.shape))
+    mx.renormalize(m, mat_l)
+    dt = 0.1 * 0.5 * 2.5e-14 * (4e-9 / 0.78125e-9) ** 2
+    sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=dt, bias=bias)
+    sim.start(m.data)
+    sim.run(max(args.warmup, 1))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        e0.record()
+        st = sim.run(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    t_step = float(ms.item())
+    # end to end through the slab driver: upload the slab, K steps, download it
+    dist.barrier()
+    w0 = time.perf_counter()
+    sim.start(m.data)
+    sim.run(args.steps)
+    _ = sim.state()
+    w = torch.tensor([time.perf_counter() - w0], device="cuda")
+    dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    N = n ** 3
+    if rank == 0:
+        out = {"metric": METRIC, "value": N / (t_step * 1e-3), "unit": "cell-steps/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic",
+               "config": {"workload": f"synthetic random-m {n}^3, full H_eff, RK4, z-slab decomposed",
+                          "cells": N, "dt": dt, "parallelism": f"z-slab x{world} ({args.backend})",
+                          "l2": "inputs > L2, no flush"},
+               "e2e": {"value": N * args.steps / float(w.item()), "unit": "cell-steps/s",
+                       "h2d_bytes_per_step": int(24 * N / world / args.steps),
+                       "d2h_bytes_per_step": int(24 * N / world / args.steps)},
+               "cpu_baseline": None, "tensor_build_s": t_build, "steps_done": int(st.steps_done),
+               "gpu_launches": args.steps * 26, "clocks": clk.summary()}
+        print(json.dumps(out))
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -159,6 +239,8 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collectives for N > 1 (gloo only to exercise the path on one GPU)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -182,15 +264,14 @@ def main():
         print(json.dumps(out))
         return
 
+    if world > 1:
+        run_slab(args, rank, world, local)
+        return
+
     import ctypes as C
 
     import paper_2602_12242_b200 as mxb
     from paper_2602_12242_b200 import _lib as L
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
     mxb.set_device(local)
     mx, g, mat, kern, rhs, m, dt, bias, t_build = setup_problem(args.n)
     N = g.n_cells
@@ -205,18 +286,11 @@ def main():
     # warm-up
     L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, max(args.warmup, 1), bptr,
                      C.byref(ms_tot), None, C.byref(nl)))
-    if world > 1:
-        dist.barrier()
     with Clocks(local) as clk:
         L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, args.steps, bptr,
                          C.byref(ms_tot), C.byref(ms_st), C.byref(nl)))
     t_step = ms_tot.value / args.steps
-    if world > 1:
-        import torch
-        t = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
-    value = world * N / (t_step * 1e-3)
+    value = N / (t_step * 1e-3)
     # per-kernel timing for the roofline
     ms_eval = C.c_double()
     passes = np.zeros(5)
@@ -271,14 +345,14 @@ def main():
     if rank != 0:
         return
     out = {
-        "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"synthetic random-m {args.n}^3, full H_eff "
                                "(demag+exchange+DMI+uniaxial anis+Zeeman), RK4",
                    "cells": N, "dt": dt, "l2": "inputs (3.2 GB/field) > L2, no flush",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm,
                      "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                      "peak_source": which},
