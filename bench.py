@@ -12,7 +12,7 @@ stage kernels).  value = cells * K / device time of K steps (CUDA events on
 the context stream, after W warm-up steps); inputs (3.2 GB per field) are
 larger than the 126 MB L2, so no explicit flush is needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--size 512] [--impl reference]
 
 Under torchrun (N>1) the 512^3 problem is z-slab decomposed over the ranks
 (strong scaling; NCCL halos, slab-FFT all-to-alls and step all-reduces); the
@@ -166,7 +166,7 @@ def run_slab(args, rank, world, local):
     torch.cuda.set_device(dev)
     mx.set_device(dev)
     dist.init_process_group(args.backend)
-    n = args.n
+    n = args.size
     plan = SlabPlan(n, n, n, world, rank)
     cell = (4e-9, 4e-9, 4e-9)
     gl = mx.GridSpec(n, n, plan.nz_local, *cell)
@@ -234,7 +234,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--size", type=int, default=512, help="cells per edge of the synthetic cube")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-n", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
@@ -256,7 +256,7 @@ def main():
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "impl": "reference",
                "config": {"workload": f"synthetic random-m {args.cpu_n}^3 full H_eff RK4 "
-                                      f"(bounded CPU sample of the {args.n}^3 workload)"},
+                                      f"(bounded CPU sample of the {args.size}^3 workload)"},
                "cpu_baseline": {"value": cs, "unit": "cell-steps/s", "cores": cores, "kind": "port",
                                 "sample": f"{args.cpu_n}^3, {args.steps} RK4 steps, oracle numpy/scipy"},
                "e2e": {"value": cs, "unit": "cell-steps/s", "h2d_bytes_per_step": 0,
@@ -273,7 +273,7 @@ def main():
     import paper_2602_12242_b200 as mxb
     from paper_2602_12242_b200 import _lib as L
     mxb.set_device(local)
-    mx, g, mat, kern, rhs, m, dt, bias, t_build = setup_problem(args.n)
+    mx, g, mat, kern, rhs, m, dt, bias, t_build = setup_problem(args.size)
     N = g.n_cells
     ctx = mat._ctx()
     L.check(ctx.call("mxb_state_set", L.dptr(m.data)))
@@ -349,7 +349,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"synthetic random-m {args.n}^3, full H_eff "
+        "config": {"workload": f"synthetic random-m {args.size}^3, full H_eff "
                                "(demag+exchange+DMI+uniaxial anis+Zeeman), RK4",
                    "cells": N, "dt": dt, "l2": "inputs (3.2 GB/field) > L2, no flush",
                    "parallelism": "single GPU"},

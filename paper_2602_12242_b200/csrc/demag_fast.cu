@@ -47,11 +47,11 @@ struct ColArgs {
     long long nlines, OS_in, OS_out;
 };
 
-template <int L, int DIR, int RM>
-__global__ void __launch_bounds__(Cfg<L, RM>::NLc * Cfg<L, RM>::TPL, 2)
+template <int L, int DIR, int RM, int NLD>
+__global__ void __launch_bounds__(Cfg<L, RM>::NLc / NLD * Cfg<L, RM>::TPL, 2)
 k_col_fast(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
-    constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NL = Cfg<L, RM>::NLc;
+    constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NL = Cfg<L, RM>::NLc / NLD;
     extern __shared__ double2 sm[];
     double2* X = sm;
     double2* S = sm + smem_elems<L, R, NL>();
@@ -425,32 +425,46 @@ static int persistent_grid(F f, int threads, size_t smem, long long ntiles, int*
     return MXB_OK;
 }
 
-template <int L, int RM>
-static int col_launch(int dir, const ColArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
-    constexpr int R = Cfg<L, RM>::R, NL = Cfg<L, RM>::NLc;
+template <int L, int RM, int NLD>
+static int col_staged(int dir, const ColArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
+    constexpr int R = Cfg<L, RM>::R, NL = Cfg<L, RM>::NLc / NLD;
     const size_t sm = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n_in) * sizeof(double2);
     const long long ntiles = (a.nlines + NL - 1) / NL;
     const int thr = NL * Cfg<L, RM>::TPL;
     int grid = 0, rc;
-    if (sm > 100 * 1024) {
-        const size_t smd = (size_t)smem_elems<L, R, NL>() * sizeof(double2);
-        if (smd > kFastSmemMax) return -1;
-        if (dir < 0) {
-            if ((rc = persistent_grid(k_col_direct<L, -1, RM>, thr, smd, 1, &grid))) return rc;
-            k_col_direct<L, -1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
-        } else {
-            if ((rc = persistent_grid(k_col_direct<L, 1, RM>, thr, smd, 1, &grid))) return rc;
-            k_col_direct<L, 1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
-        }
-        MXB_LAUNCH_CHECK();
-        return MXB_OK;
-    }
     if (dir < 0) {
-        if ((rc = persistent_grid(k_col_fast<L, -1, RM>, thr, sm, ntiles, &grid))) return rc;
-        k_col_fast<L, -1, RM><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_col_fast<L, -1, RM, NLD>, thr, sm, ntiles, &grid))) return rc;
+        k_col_fast<L, -1, RM, NLD><<<grid, thr, sm, st>>>(a, tw, halt);
     } else {
-        if ((rc = persistent_grid(k_col_fast<L, 1, RM>, thr, sm, ntiles, &grid))) return rc;
-        k_col_fast<L, 1, RM><<<grid, thr, sm, st>>>(a, tw, halt);
+        if ((rc = persistent_grid(k_col_fast<L, 1, RM, NLD>, thr, sm, ntiles, &grid))) return rc;
+        k_col_fast<L, 1, RM, NLD><<<grid, thr, sm, st>>>(a, tw, halt);
+    }
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+template <int L, int RM>
+static int col_launch(int dir, const ColArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
+    constexpr int R = Cfg<L, RM>::R, NL = Cfg<L, RM>::NLc;
+    const size_t full = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n_in) * sizeof(double2);
+    // staged (cp.async prefetch of the next tile) whenever two CTAs fit on an SM;
+    // halve the lines per CTA for long inputs (the inverse pass reads all L rows)
+    if (full <= 110 * 1024) return col_staged<L, RM, 1>(dir, a, tw, st, halt);
+    if (NL >= 4) {
+        const size_t half = ((size_t)smem_elems<L, R, NL / 2>() + (size_t)(NL / 2) * a.n_in) * sizeof(double2);
+        if (half <= 110 * 1024) return col_staged<L, RM, 2>(dir, a, tw, st, halt);
+    }
+    const long long ntiles = (a.nlines + NL - 1) / NL;
+    const int thr = NL * Cfg<L, RM>::TPL;
+    int grid = 0, rc;
+    const size_t smd = (size_t)smem_elems<L, R, NL>() * sizeof(double2);
+    if (smd > kFastSmemMax) return -1;
+    if (dir < 0) {
+        if ((rc = persistent_grid(k_col_direct<L, -1, RM>, thr, smd, 1, &grid))) return rc;
+        k_col_direct<L, -1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
+    } else {
+        if ((rc = persistent_grid(k_col_direct<L, 1, RM>, thr, smd, 1, &grid))) return rc;
+        k_col_direct<L, 1, RM><<<(unsigned)ntiles, thr, smd, st>>>(a, tw, halt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
