@@ -55,8 +55,8 @@ enum {
 /* ghost modes of _StencilPlan (fields.py:18,49-92) */
 enum { MXB_GHOST_NEUMANN = 0, MXB_GHOST_DMI = 1, MXB_GHOST_PERIODIC = 2 };
 
-/* integrators (llg.py:206-222) */
-enum { MXB_EULER = 0, MXB_RK4 = 1 };
+/* integrators (llg.py:206-222; MRI = explicit multirate Knoth-Wolke, integrators.py:97-128) */
+enum { MXB_EULER = 0, MXB_RK4 = 1, MXB_MRI_KW3 = 2 };
 
 /* GridSpec (grid.py:29-71) */
 typedef struct mxb_grid {
@@ -167,14 +167,21 @@ int mxb_state_get(mxb_ctx* ctx, double* m);
 /* per-stage uniform bias for the next nsteps (rows of 3 doubles, nsteps x
  * stages-per-step), or NULL to use the constant b->vec of mxb_run */
 typedef struct mxb_run_args {
-    int32_t method;            /* MXB_EULER / MXB_RK4 */
+    int32_t method;            /* MXB_EULER / MXB_RK4 / MXB_MRI_KW3 */
     int32_t renorm_each_stage; /* IntegratorSpec.renorm_each_stage */
     double dt;
     int64_t nsteps;            /* steps to attempt in this call */
     double eq_tol;             /* < 0: no equilibrium stop */
-    const double* stage_bias;  /* host (nsteps*stages*3) or NULL */
+    /* host rows of 3 doubles, one per right-hand-side evaluation that needs the
+     * bias, in evaluation order (RK4: 4 per step at t, t+dt/2, t+dt/2, t+dt;
+     * Euler: 1; MRI: the slow or fast evaluations of the partition holding the
+     * bias), or NULL for the constant bias_vec */
+    const double* stage_bias;
     const double* bias_field;  /* host (3,nz,ny,nx) static spatial bias or NULL */
     double bias_vec[3];        /* constant uniform bias (if stage_bias NULL) */
+    uint32_t fast_mask;        /* MRI: terms in the fast partition (llg.py:41-47) */
+    int32_t pad;
+    double theta;              /* MRI: fast step ratio (IntegratorSpec.theta) */
 } mxb_run_args;
 typedef struct mxb_run_stats {
     int64_t steps_done;        /* committed steps */

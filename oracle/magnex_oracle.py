@@ -564,6 +564,70 @@ def rk4_step(y, t, dt, f, post=None):
     return y + (dt / 6.0) * (k1 + 2.0 * (k2 + k3) + k4)
 
 
+# Knoth-Wolke tableau and multirate forcing weights (integrators.py:28-40)
+KW3_C = (0.0, 1.0 / 3.0, 3.0 / 4.0)
+KW3_A = ((0.0, 0.0, 0.0), (1.0 / 3.0, 0.0, 0.0), (-3.0 / 16.0, 15.0 / 16.0, 0.0))
+KW3_B = (1.0 / 6.0, 3.0 / 10.0, 8.0 / 15.0)
+MRI_DC = (1.0 / 3.0, 5.0 / 12.0, 1.0 / 4.0)
+MRI_W = ((1.0,), (-5.0 / 4.0, 9.0 / 4.0), (17.0 / 12.0, -51.0 / 20.0, 32.0 / 15.0))
+
+
+def kw3_step(y, t, dt, f, post=None):
+    """Three-stage third-order step (integrators.py:67-78)."""
+    k1 = f(t, y)
+    y2 = y + (dt * KW3_A[1][0]) * k1
+    y2 = post(y2) if post else y2
+    k2 = f(t + KW3_C[1] * dt, y2)
+    y3 = y + dt * (KW3_A[2][0] * k1 + KW3_A[2][1] * k2)
+    y3 = post(y3) if post else y3
+    k3 = f(t + KW3_C[2] * dt, y3)
+    return y + dt * (KW3_B[0] * k1 + KW3_B[1] * k2 + KW3_B[2] * k3)
+
+
+def substeps(theta):
+    """ceil(delta-c / theta) fast substeps per slow phase (integrators.py:81-89)."""
+    return tuple(math.ceil(dc / theta - 1e-12) for dc in MRI_DC)
+
+
+def mri_kw3_step(y, t, dt, f_slow, f_fast, theta=0.1, post=None):
+    """Explicit multirate step: 3 slow evaluations, KW3-subcycled fast system
+    under piecewise-constant slow forcing (integrators.py:97-128)."""
+    n = substeps(theta)
+    fs = [f_slow(t, y)]
+    v = y
+    for ph in range(3):
+        w = MRI_W[ph]
+        r = w[0] * fs[0]
+        for j in range(1, len(w)):
+            r = r + w[j] * fs[j]
+        h = MRI_DC[ph] * dt / n[ph]
+        t0 = t + KW3_C[ph] * dt
+        for s in range(n[ph]):
+            v = kw3_step(v, t0 + s * h, h, lambda tt, vv, r=r: f_fast(tt, vv) + r, post)
+            v = post(v) if post else v
+        if ph < 2:
+            fs.append(f_slow(t + KW3_C[ph + 1] * dt, v))
+    return v
+
+
+def split_terms(terms: Terms, fast: set):
+    """(slow, fast) Terms of a partition (llg.py:127-136,183-189)."""
+    import dataclasses
+    on = {"exchange": terms.exchange, "anisotropy": terms.anisotropy, "dmi": terms.dmi,
+          "demag": terms.spectra is not None, "bias": terms.bias is not None}
+    mode = terms.mode()
+
+    def pick(keep):
+        return dataclasses.replace(
+            terms, exchange=on["exchange"] and "exchange" in keep,
+            anisotropy=on["anisotropy"] and "anisotropy" in keep, dmi=on["dmi"] and "dmi" in keep,
+            spectra=terms.spectra if "demag" in keep else None,
+            bias=terms.bias if "bias" in keep else None, ghost_mode=mode)
+
+    all_terms = set(on)
+    return pick(all_terms - fast), pick(fast)
+
+
 def energies(t, m, mat: Mat, terms: Terms, plan: Plan | None = None):
     """(e_demag, e_exch, e_anis, e_zeeman), means over magnetic cells
     (fields.py:200-242 via llg.py:201-203)."""
@@ -610,12 +674,20 @@ class RunResult:
 
 def run(m0, mat: Mat, terms: Terms, method: str, dt: float, *, t0=0.0, step0=0,
         max_time=None, max_steps=None, eq_tol=None, renorm_each_stage=True,
-        sample_every=10 ** 9, with_energies=False) -> RunResult:
+        sample_every=10 ** 9, with_energies=False, theta=0.1, fast=("exchange",)) -> RunResult:
     """Fixed-step driver loop of Simulation.run_until (llg.py:320-379)."""
     plan = Plan(mat, terms.mode())
 
     def f(t, y):
         return rhs_total(t, y, mat, terms, plan)
+
+    slow_t, fast_t = split_terms(terms, set(fast))
+
+    def f_slow(t, y):
+        return rhs_total(t, y, mat, slow_t, plan)
+
+    def f_fast(t, y):
+        return rhs_total(t, y, mat, fast_t, plan)
 
     def post(y):
         return renormalize(y, mat)
@@ -649,6 +721,10 @@ def run(m0, mat: Mat, terms: Terms, method: str, dt: float, *, t0=0.0, step0=0,
         elif method == "rk4":
             y = rk4_step(res.m, res.t, dt, f, post if renorm_each_stage else None)
             res.evals += 4
+        elif method == "mri-kw3":
+            y = mri_kw3_step(res.m, res.t, dt, f_slow, f_fast, theta,
+                             post if renorm_each_stage else None)
+            res.evals += 3
         else:
             raise ValueError(method)
         nrm = np.sqrt(np.einsum("cijk,cijk->ijk", y, y))[mask]

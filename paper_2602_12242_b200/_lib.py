@@ -18,7 +18,7 @@ OK, EINVAL, EDEAD, EBLOWUP, ECUDA, ENCCL, EQUILIBRATED = 0, 1, 2, 3, 4, 5, 6
 TERM_EXCHANGE, TERM_ANISOTROPY, TERM_DMI, TERM_DEMAG, TERM_BIAS, TERM_CUBIC, TERM_BULK_DMI = (
     1, 2, 4, 8, 16, 32, 64)
 GHOST = {"neumann": 0, "dmi": 1, "periodic": 2}
-EULER, RK4 = 0, 1
+EULER, RK4, MRI_KW3 = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
 
@@ -49,7 +49,8 @@ class Bias(C.Structure):
 class RunArgs(C.Structure):
     _fields_ = [("method", C.c_int32), ("renorm_each_stage", C.c_int32), ("dt", C.c_double),
                 ("nsteps", C.c_int64), ("eq_tol", C.c_double), ("stage_bias", _dp),
-                ("bias_field", _dp), ("bias_vec", C.c_double * 3)]
+                ("bias_field", _dp), ("bias_vec", C.c_double * 3), ("fast_mask", C.c_uint32),
+                ("pad", C.c_int32), ("theta", C.c_double)]
 
 
 class StageIO(C.Structure):

@@ -2,6 +2,7 @@
 // operator calls, and the device-resident stepping loop that replaces the
 // body of Simulation.run_until (llg.py:320-379).
 #include <limits.h>
+#include <math.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -58,6 +59,7 @@ struct mxb_ctx {
     double* tA = nullptr;
     double* tB = nullptr;
     double* bias_dev = nullptr;   // (3,N) spatial bias scratch
+    double* mri[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // F0..F2, R, V, K2, K3
     Ctl* ctl = nullptr;
     double* partials = nullptr;
     bool state_valid = false;
@@ -187,6 +189,7 @@ int mxb_ctx_destroy(mxb_ctx* c) {
     if (c->st) cudaStreamSynchronize(c->st);
     double* bufs[] = {c->mat_buf, c->Yb[0], c->Yb[1], c->P, c->K1, c->S, c->Hd, c->tA, c->tB, c->bias_dev, c->partials};
     for (double* b : bufs) if (b) cudaFree(b);
+    for (double* b : c->mri) if (b) cudaFree(b);
     if (c->ctl) cudaFree(c->ctl);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -700,11 +703,121 @@ static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int metho
     return launch_stage(M_RK4, c->exact, a, c->st);
 }
 
+// ---------------------------------------------------------------------------
+// multirate Knoth-Wolke step (integrators.py:29-40,67-128)
+// ---------------------------------------------------------------------------
+static const double kKW3_C[3] = {0.0, 1.0 / 3.0, 3.0 / 4.0};
+static const double kKW3_A10 = 1.0 / 3.0, kKW3_A20 = -3.0 / 16.0, kKW3_A21 = 15.0 / 16.0;
+static const double kKW3_B[3] = {1.0 / 6.0, 3.0 / 10.0, 8.0 / 15.0};
+static const double kMRI_DC[3] = {1.0 / 3.0, 5.0 / 12.0, 1.0 / 4.0};
+static const double kMRI_W[3][3] = {{1.0, 0.0, 0.0},
+                                    {-5.0 / 4.0, 9.0 / 4.0, 0.0},
+                                    {17.0 / 12.0, -51.0 / 20.0, 32.0 / 15.0}};
+
+int mri_substeps(double theta, int n[3]) {
+    for (int i = 0; i < 3; ++i) n[i] = (int)ceil(kMRI_DC[i] / theta - 1e-12);
+    return n[0] + n[1] + n[2];
+}
+
+static int enqueue_step_mri(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, uint32_t mask,
+                            uint32_t fast_mask, double dt, double theta, const double* rows,
+                            int* row_i, bool renorm) {
+    const uint32_t slow_mask = mask & ~fast_mask;
+    const bool bias_fast = (fast_mask & MXB_TERM_BIAS) != 0;
+    double* y = c->Yb[c->cur];
+    double* ynew = c->Yb[c->cur ^ 1];
+    double* F[3] = {c->mri[0], c->mri[1], c->mri[2]};
+    double *R = c->mri[3], *V = c->mri[4], *K1m = c->K1, *K2m = c->mri[5], *K3m = c->mri[6];
+    double* YS = c->P;
+    const int* halt = &c->ctl->halt;
+    const size_t fb = fbytes(c->g);
+    int rc;
+    auto rhs = [&](uint32_t m, const double* ys, double* out, bool is_fast) -> int {
+        StageArgs a = a0;
+        a.halt = halt;
+        a.terms = m;
+        a.ys = ys;
+        a.out = out;
+        if ((m & MXB_TERM_BIAS) && rows && (is_fast == bias_fast)) {
+            for (int q = 0; q < 3; ++q) a.bias[q] = rows[3 * (*row_i) + q];
+            ++*row_i;
+        }
+        if (m & MXB_TERM_DEMAG) {
+            int r = demag_into(c, d, ys, c->Hd, halt);
+            if (r) return r;
+            a.hd = c->Hd;
+        }
+        return launch_stage(M_RHS, c->exact, a, c->st, false);
+    };
+    auto comb = [&](double* out, const double* base, int n, const double* const* x, const double* cf,
+                    bool rn) -> int {
+        StageArgs a = a0;
+        a.halt = halt;
+        CombArgs cb{};
+        cb.out = out;
+        cb.base = base;
+        cb.n = n;
+        for (int i = 0; i < n; ++i) { cb.x[i] = x[i]; cb.c[i] = cf[i]; }
+        cb.renorm = rn ? 1 : 0;
+        return launch_comb(c->exact, a, cb, c->st);
+    };
+    int nsub[3];
+    mri_substeps(theta, nsub);
+    if ((rc = rhs(slow_mask, y, F[0], false))) return rc;
+    MXB_CUDA(cudaMemcpyAsync(V, y, fb, cudaMemcpyDeviceToDevice, c->st));
+    for (int ph = 0; ph < 3; ++ph) {
+        {   // piecewise-constant slow forcing r = sum_j w_j f_j
+            const double* xs[3] = {F[0], F[1], F[2]};
+            if ((rc = comb(R, nullptr, ph + 1, xs, kMRI_W[ph], false))) return rc;
+        }
+        const double h = kMRI_DC[ph] * dt / nsub[ph];
+        for (int s = 0; s < nsub[ph]; ++s) {
+            const double one = 1.0;
+            const double* rx[1] = {R};
+            if ((rc = rhs(fast_mask, V, K1m, true))) return rc;
+            if ((rc = comb(K1m, K1m, 1, rx, &one, false))) return rc;
+            {
+                const double* xs[1] = {K1m};
+                const double cf[1] = {h * kKW3_A10};
+                if ((rc = comb(YS, V, 1, xs, cf, renorm))) return rc;
+            }
+            if ((rc = rhs(fast_mask, YS, K2m, true))) return rc;
+            if ((rc = comb(K2m, K2m, 1, rx, &one, false))) return rc;
+            {
+                const double* xs[2] = {K1m, K2m};
+                const double cf[2] = {h * kKW3_A20, h * kKW3_A21};
+                if ((rc = comb(YS, V, 2, xs, cf, renorm))) return rc;
+            }
+            if ((rc = rhs(fast_mask, YS, K3m, true))) return rc;
+            if ((rc = comb(K3m, K3m, 1, rx, &one, false))) return rc;
+            {
+                const double* xs[3] = {K1m, K2m, K3m};
+                const double cf[3] = {h * kKW3_B[0], h * kKW3_B[1], h * kKW3_B[2]};
+                if ((rc = comb(V, V, 3, xs, cf, renorm))) return rc;
+            }
+        }
+        if (ph < 2 && (rc = rhs(slow_mask, V, F[ph + 1], false))) return rc;
+    }
+    (void)kKW3_C;
+    StageArgs a = a0;
+    a.halt = halt;
+    return launch_final_state(c->exact, a, V, ynew, c->st);
+}
+
 int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra,
             mxb_run_stats* st) {
     if (!c || !t || !ra || !st) { set_error("null argument"); return MXB_EINVAL; }
     if (!c->state_valid) { set_error("no resident state"); return MXB_EINVAL; }
-    if (ra->method != MXB_EULER && ra->method != MXB_RK4) { set_error("unknown method"); return MXB_EINVAL; }
+    if (ra->method != MXB_EULER && ra->method != MXB_RK4 && ra->method != MXB_MRI_KW3) {
+        set_error("unknown method");
+        return MXB_EINVAL;
+    }
+    if (ra->method == MXB_MRI_KW3) {
+        const uint32_t fm = ra->fast_mask & t->mask;
+        if (!fm) { set_error("multirate stepping needs a non-empty fast partition"); return MXB_EINVAL; }
+        if (!(t->mask & ~fm)) { set_error("multirate stepping needs a non-empty slow partition"); return MXB_EINVAL; }
+        if (!(ra->theta > 0.0 && ra->theta <= 1.0)) { set_error("theta must be in (0, 1]"); return MXB_EINVAL; }
+    }
     cudaSetDevice(c->dev);
     const bool use_demag = (t->mask & MXB_TERM_DEMAG) != 0;
     int rc;
@@ -734,9 +847,19 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     }
     const int stages = ra->method == MXB_RK4 ? 4 : 1;
     const int start = c->cur;
+    if (ra->method == MXB_MRI_KW3) {
+        for (int i = 0; i < 7; ++i)
+            if ((rc = ensure(&c->mri[i], fbytes(c->g)))) return rc;
+    }
+    int row_i = 0;
     for (int64_t k = 0; k < ra->nsteps; ++k) {
-        const double* sb = ra->stage_bias ? ra->stage_bias + (size_t)k * stages * 3 : nullptr;
-        rc = enqueue_step(c, d, a, ra->method, ra->dt, sb, ra->renorm_each_stage != 0, use_demag);
+        if (ra->method == MXB_MRI_KW3) {
+            rc = enqueue_step_mri(c, d, a, t->mask, ra->fast_mask & t->mask, ra->dt, ra->theta,
+                                  ra->stage_bias, &row_i, ra->renorm_each_stage != 0);
+        } else {
+            const double* sb = ra->stage_bias ? ra->stage_bias + (size_t)k * stages * 3 : nullptr;
+            rc = enqueue_step(c, d, a, ra->method, ra->dt, sb, ra->renorm_each_stage != 0, use_demag);
+        }
         if (rc) return rc;
         c->cur ^= 1;
     }

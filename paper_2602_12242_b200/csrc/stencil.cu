@@ -705,6 +705,88 @@ int launch_renorm(const StageArgs& a, double* m, cudaStream_t st) {
     return MXB_OK;
 }
 
+// out = base + sum_i c[i] * x[i] (i < n <= 4), then optionally the
+// renormalisation hook (grid.py:178-200) -- the stage arithmetic of the
+// Knoth-Wolke / multirate steps (integrators.py:67-128)
+template <bool E, bool U>
+__global__ void __launch_bounds__(256) k_comb(StageArgs a, CombArgs cb) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    const long long N = a.g.N;
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= N) return;
+    double v[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double acc = cb.base ? cb.base[q * N + idx] : 0.0;
+        for (int i = 0; i < cb.n; ++i) acc = add<E>(acc, mul<E>(cb.c[i], cb.x[i][q * N + idx]));
+        v[q] = acc;
+    }
+    if (cb.renorm) {
+        const CellMat cm = cell_mat<E, U>(a, idx);
+        if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cb.out[q * N + idx] = v[q];
+}
+
+// end of a step computed elsewhere: pre-renormalisation drift, renormalise
+// into out, <m> partials (llg.py:347-362); followed by k_finalize(mode 0)
+template <bool E, bool U>
+__global__ void __launch_bounds__(256) k_final_state(StageArgs a, const double* vin, double* out) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    const long long N = a.g.N;
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    if (idx < N) {
+        const CellMat cm = cell_mat<E, U>(a, idx);
+        double v[3] = {vin[idx], vin[N + idx], vin[2 * N + idx]};
+        if (cm.mag) {
+            const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
+            double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
+            if (!(d == d) || isinf(d)) d = DBL_MAX;
+            red[3] = d;
+        }
+        if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
+        if (cm.mag)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) red[q] = E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms);
+        out[idx] = v[0]; out[N + idx] = v[1]; out[2 * N + idx] = v[2];
+    }
+    const bool is_max[4] = {false, false, false, true};
+    block_reduce<4>(red, is_max);
+    if (threadIdx.x == 0) {
+        double* p = a.partials + (long long)blockIdx.x * kReduceSlots;
+        p[0] = red[0]; p[1] = red[1]; p[2] = red[2]; p[3] = red[3];
+    }
+}
+
+int launch_comb(bool exact, const StageArgs& a, const CombArgs& cb, cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    if (exact) {
+        if (a.mat.uniform) k_comb<true, true><<<nb, kBlock, 0, st>>>(a, cb);
+        else k_comb<true, false><<<nb, kBlock, 0, st>>>(a, cb);
+    } else {
+        if (a.mat.uniform) k_comb<false, true><<<nb, kBlock, 0, st>>>(a, cb);
+        else k_comb<false, false><<<nb, kBlock, 0, st>>>(a, cb);
+    }
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+int launch_final_state(bool exact, const StageArgs& a, const double* vin, double* out,
+                       cudaStream_t st) {
+    const int nb = stage_blocks(a.g.N);
+    if (exact) {
+        if (a.mat.uniform) k_final_state<true, true><<<nb, kBlock, 0, st>>>(a, vin, out);
+        else k_final_state<true, false><<<nb, kBlock, 0, st>>>(a, vin, out);
+    } else {
+        if (a.mat.uniform) k_final_state<false, true><<<nb, kBlock, 0, st>>>(a, vin, out);
+        else k_final_state<false, false><<<nb, kBlock, 0, st>>>(a, vin, out);
+    }
+    MXB_LAUNCH_CHECK();
+    return launch_finalize(a, 0, st);
+}
+
 template <bool U>
 __global__ void k_mean(StageArgs a, const double* m) {
     const long long N = a.g.N;

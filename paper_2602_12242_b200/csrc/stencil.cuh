@@ -65,6 +65,18 @@ struct StageArgs {
 };
 
 int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st, bool finalize = true);
+// out = base + sum_i c[i] * x[i] (i < n <= 4), optionally renormalised
+struct CombArgs {
+    double* out;
+    const double* base;
+    const double* x[4];
+    double c[4];
+    int n;
+    int renorm;
+};
+int launch_comb(bool exact, const StageArgs& a, const CombArgs& cb, cudaStream_t st);
+int launch_final_state(bool exact, const StageArgs& a, const double* vin, double* out,
+                       cudaStream_t st);
 int launch_term(uint32_t term, int ghost, bool exact, const StageArgs& a, cudaStream_t st);
 int launch_renorm(const StageArgs& a, double* m, cudaStream_t st);
 int launch_mean(const StageArgs& a, const double* m, cudaStream_t st);

@@ -21,7 +21,8 @@ from .demag import DemagKernel
 from .fields import (AnisotropyOperator, BulkDmiOperator, CubicAnisotropyOperator, DmiOperator,
                      EnergyBreakdown, ExchangeOperator, _StencilPlan)
 from .grid import MaterialMap, RenormalizeError, VectorField3, _raise_dead, mean_normalized, renormalize
-from .integrators import euler_step, fast_evals_per_step, mri_kw3_step, rk4_step
+from .integrators import (_MRI_DC, KW3_C, euler_step, fast_evals_per_step, mri_kw3_step, rk4_step,
+                          substeps_per_phase)
 
 __all__ = ["SLOW_EXPLICIT", "FAST", "SLOW_IMPLICIT", "TERMS", "llg_rhs", "PartitionedRHS",
            "IntegratorSpec", "StopCondition", "SimState", "Trajectory", "Simulation",
@@ -371,9 +372,34 @@ class Simulation:
             n_total = stop.max_steps if n_total is None else min(n_total, stop.max_steps)
         return n_total
 
+    def _bias_times(self, t: float):
+        """Times of the right-hand-side evaluations that read the bias in one
+        step from t, in evaluation order (integrators.py:43-128)."""
+        sp = self.ispec
+        dt = sp.dt
+        if sp.method == "euler":
+            return [t]
+        if sp.method == "rk4":
+            half = 0.5 * dt
+            return [t, t + half, t + half, t + dt]
+        slow = self.rhs.partition.get("bias", SLOW_EXPLICIT) == SLOW_EXPLICIT
+        nsub = substeps_per_phase(sp.theta)
+        times = [t] if slow else []
+        for ph in range(3):
+            if not slow:
+                span = _MRI_DC[ph] * dt
+                t0 = t + KW3_C[ph] * dt
+                h = span / nsub[ph]
+                for s in range(nsub[ph]):
+                    ts = t0 + s * h
+                    times += [ts, ts + KW3_C[1] * h, ts + KW3_C[2] * h]
+            if ph < 2 and slow:
+                times.append(t + KW3_C[ph + 1] * dt)
+        return times
+
     def run_until(self, stop: StopCondition) -> Trajectory:
         rhs, sp = self.rhs, self.ispec
-        device = sp.method in ("euler", "rk4") and rhs._device_ok()
+        device = sp.method in ("euler", "rk4", "mri-kw3") and rhs._device_ok()
         b0 = None
         if device and rhs._bias is not None and not callable(rhs._bias):
             b0 = rhs.bias_at(0.0)
@@ -413,8 +439,6 @@ class Simulation:
         reason = "max_time" if stop.max_time is not None else "max_steps"
         if n_total is not None and stop.max_steps is not None and n_total == stop.max_steps:
             reason = "max_steps"
-        stages = 4 if sp.method == "rk4" else 1
-        offs = (0.0, 0.5, 0.5, 1.0) if stages == 4 else (0.0,)
         terms = rhs.enabled_terms()
         ts = rhs._terms_struct(tuple(x for x in _ORDER if x in terms))
         evals = self._evals_per_step()
@@ -422,7 +446,9 @@ class Simulation:
         eq = stop.equilibrium_tol
         keep = []
         args = L.RunArgs()
-        args.method = L.RK4 if sp.method == "rk4" else L.EULER
+        args.method = {"rk4": L.RK4, "euler": L.EULER, "mri-kw3": L.MRI_KW3}[sp.method]
+        args.theta = sp.theta
+        args.fast_mask = sum(_BIT[x] for x in terms if rhs.partition[x] == FAST)
         args.renorm_each_stage = 1 if sp.renorm_each_stage else 0
         args.dt = sp.dt
         args.eq_tol = float(eq) if eq is not None else -1.0
@@ -440,12 +466,9 @@ class Simulation:
             to_sample = self.sample_every - (k % self.sample_every)
             chunk = min(n_total - k, to_sample, self.CHUNK_EQ if eq is not None else self.CHUNK)
             if callable(rhs._bias):
-                half = 0.5 * sp.dt
                 rows = []
                 for s in range(chunk):
-                    t = t0 + (k + s) * sp.dt
-                    for o in offs:
-                        tt = t if o == 0.0 else (t + half if o == 0.5 else t + sp.dt)
+                    for tt in self._bias_times(t0 + (k + s) * sp.dt):
                         v = rhs.bias_at(tt)
                         if v.shape != (3,):
                             raise NotImplementedError(

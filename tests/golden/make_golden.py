@@ -38,7 +38,8 @@ def sha(a: np.ndarray) -> str:
 
 
 def case(name, dims, cell, mat_kw, terms, seed, *, ghost_mode=None, bias=None,
-         demag=False, dt=1e-13, nsteps=0, method="rk4", msmap=None, store_tensor=True):
+         demag=False, dt=1e-13, nsteps=0, method="rk4", msmap=None, store_tensor=True,
+         mri_steps=0):
     nx, ny, nz = dims
     g = GridSpec(nx, ny, nz, *cell)
     kw = dict(mat_kw)
@@ -89,6 +90,17 @@ def case(name, dims, cell, mat_kw, terms, seed, *, ghost_mode=None, bias=None,
         out["trace_final"] = st.m.data.copy() if g.n_cells <= 20000 else np.zeros(0)
         out["trace_final_sha"] = sha(st.m.data)
         out["trace_method"] = method
+        if bool(mri_steps) and "exchange" in terms:
+            rhs.counters = {k: 0 for k in rhs.counters}
+            st = SimState(VectorField3(g, m0.copy()))
+            sim = Simulation(st, rhs, IntegratorSpec("mri-kw3", 4 * dt), sample_every=1,
+                             energy_in_samples=False)
+            tr = sim.run_until(StopCondition(max_steps=mri_steps))
+            out["mri_dt"] = 4 * dt
+            out["mri_trace_m"] = np.stack([tr.column("mx"), tr.column("my"), tr.column("mz")], 1)
+            out["mri_final"] = st.m.data.copy()
+            out["mri_counters"] = np.array([tr.counters.get(k, 0) for k in
+                                            ("exchange", "anisotropy", "dmi", "demag", "bias")])
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **out)
     print(name, "ok", {k: (v.shape if hasattr(v, "shape") else v) for k, v in out.items()
                        if k.startswith(("h_", "rk4", "trace_m"))})
@@ -106,7 +118,7 @@ def main():
     # tiny grids: every term, every boundary mode
     case("box_6x5x4_all", (6, 5, 4), (1e-9, 2e-9, 1.5e-9),
          dict(Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.3, 0.2, 1.0), D=1e-3, alpha=0.1),
-         ALL, 1, bias=(1e4, -2e3, 5e3), demag=True, dt=2e-14, nsteps=10)
+         ALL, 1, bias=(1e4, -2e3, 5e3), demag=True, dt=2e-14, nsteps=10, mri_steps=4)
     case("box_6x5x4_neumann", (6, 5, 4), (1e-9, 2e-9, 1.5e-9),
          dict(Ms=8e5, A=1.3e-11, Ku=5e4, alpha=0.02),
          ("exchange", "anisotropy"), 2, bias=(1e4, 0.0, 0.0), demag=True, dt=2e-14, nsteps=10)
@@ -118,7 +130,7 @@ def main():
          bias=(0.0, 5e3, 0.0), demag=True, dt=2e-14, nsteps=5)
     case("film_4x4x1", (4, 4, 1), (2e-9, 2e-9, 2e-9),
          dict(Ms=8e5, A=1.3e-11, alpha=0.1), ("exchange",), 7, bias=(0.0, 0.0, 1e4),
-         demag=True, dt=2.5e-14, nsteps=5)
+         demag=True, dt=2.5e-14, nsteps=5, mri_steps=3)
     case("chain_8x1x1", (8, 1, 1), (2e-9, 1e-9, 3e-9),
          dict(Ms=8e5, A=1.3e-11, D=2e-3, alpha=0.2), ("exchange", "dmi"), 8,
          demag=True, dt=1e-14, nsteps=3)
@@ -129,7 +141,7 @@ def main():
          dt=1e-13, nsteps=5)
     case("disk_16_dmi", (16, 16, 1), (1e-9, 1e-9, 0.25e-9),
          dict(A=16e-12, Ku=5.5e5, D=4.5e-3, alpha=1.0), ALL, 11, msmap=disk,
-         dt=1e-14, nsteps=10)
+         dt=1e-14, nsteps=10, mri_steps=3)
     case("disk_16_dmi_demag", (16, 16, 2), (1e-9, 1e-9, 0.5e-9),
          dict(A=16e-12, Ku=5.5e5, D=4.5e-3, alpha=0.5), ALL, 12, msmap=disk, demag=True,
          dt=1e-14, nsteps=5)

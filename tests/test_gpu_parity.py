@@ -200,3 +200,61 @@ def test_symmetric_quarter_kernel(dims):
     m = np.random.default_rng(6).normal(size=(3,) + g.shape) * 8e5
     ref = O.demag_field(spec, m)
     assert nrm(ks.field(m), ref) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["box_6x5x4_all", "film_4x4x1", "disk_16_dmi"])
+def test_mri_device_trace(name, mode):
+    """Device multirate KW3 vs the reference trace and counters."""
+    z = load(name)
+    g, mat, rhs, kern = build(z)
+    n = len(z["mri_trace_m"]) - 1
+    st = mx.SimState(mx.VectorField3(g, z["m0"].copy()))
+    sim = mx.Simulation(st, rhs, mx.IntegratorSpec("mri-kw3", float(z["mri_dt"])), sample_every=1,
+                        energy_in_samples=False)
+    tr = sim.run_until(mx.StopCondition(max_steps=n))
+    got = np.stack([tr.column("mx"), tr.column("my"), tr.column("mz")], 1)
+    assert np.max(np.abs(got - z["mri_trace_m"])) <= 1e-10
+    assert nrm(st.m.data, z["mri_final"]) <= 1e-10
+    want = dict(zip(("exchange", "anisotropy", "dmi", "demag", "bias"), z["mri_counters"]))
+    for k, v in tr.counters.items():
+        assert v == want[k], (k, v, want[k])
+
+
+def test_mri_single_spin_third_order():
+    """integrators convergence (test_llg.py:122-139 analogue): MRI order 3 +- 0.2."""
+    import math
+    MS, h0, alpha, t_end = 8e5, 7.9577e5, 0.2, 4e-12
+
+    def closed(t):
+        gl = 1.759e11 / (1.0 + alpha * alpha)
+        om = gl * mx.MU0 * h0
+        th = 2.0 * math.atan(math.exp(-alpha * om * t))
+        return MS * np.array([math.sin(th) * math.cos(om * t), math.sin(th) * math.sin(om * t),
+                              math.cos(th)])
+
+    errs = []
+    for dt in (4e-13, 2e-13, 1e-13):
+        g = mx.GridSpec(1, 1, 1, 1e-9, 1e-9, 1e-9)
+        mat = mx.MaterialMap(g, Ms=MS, alpha=alpha, A=1.3e-11)
+        rhs = mx.PartitionedRHS(mat, exchange=True, bias=(0.0, 0.0, h0))
+        st = mx.SimState(mx.VectorField3.from_uniform(g, (MS, 0.0, 0.0)))
+        sim = mx.Simulation(st, rhs, mx.IntegratorSpec("mri-kw3", dt, renorm_each_stage=False),
+                            sample_every=10 ** 9, energy_in_samples=False)
+        sim.run_until(mx.StopCondition(max_time=t_end))
+        errs.append(np.max(np.abs(st.m.data[:, 0, 0, 0] - closed(t_end))) / MS)
+    order = math.log2(errs[1] / errs[2])
+    assert abs(order - 3.0) < 0.2, errs
+
+
+def test_mri_counter_contract():
+    """3 demag and 36 exchange evaluations per multirate step at theta = 0.1
+    (test_llg.py:166-175)."""
+    z = load("film_4x4x1")
+    g, mat, rhs, kern = build(z)
+    st = mx.SimState(mx.VectorField3(g, z["m0"].copy()))
+    sim = mx.Simulation(st, rhs, mx.IntegratorSpec("mri-kw3", 1.25e-13, theta=0.1),
+                        sample_every=10 ** 9, energy_in_samples=False)
+    tr = sim.run_until(mx.StopCondition(max_time=1.25e-13))
+    assert st.step == 1
+    assert tr.counters["demag"] == 3 and tr.counters["bias"] == 3
+    assert tr.counters["exchange"] == 36

@@ -99,3 +99,17 @@ def test_sp4_protocol_trace():
     assert np.array_equal(np.array([row["mx"] for row in r.rows]), z["mx"])
     assert np.array_equal(np.array([row["e_total"] for row in r.rows]), z["e_total"])
     assert sha(r.m) == str(z["final_sha"])
+
+
+@pytest.mark.parametrize("name", ["box_6x5x4_all", "film_4x4x1", "disk_16_dmi"])
+def test_mri_trace_bit_exact(name):
+    """Multirate KW3 (integrators.py:97-128) through the run loop, vs the reference."""
+    z = load(name)
+    mat = mat_of(z)
+    spectra = O.kernel_spectra(packed_of(z)) if bool(z["has_demag"]) else None
+    terms = terms_of(z, spectra)
+    n = len(z["mri_trace_m"]) - 1
+    r = O.run(z["m0"], mat, terms, "mri-kw3", float(z["mri_dt"]), max_steps=n, sample_every=1)
+    got = np.array([[row["mx"], row["my"], row["mz"]] for row in r.rows])
+    assert np.array_equal(got, z["mri_trace_m"])
+    assert np.array_equal(r.m, z["mri_final"])
