@@ -3,7 +3,9 @@
 // body of Simulation.run_until (llg.py:320-379).
 #include <limits.h>
 #include <math.h>
+#include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -32,10 +34,13 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 
 using namespace mxb;
 
+static uint64_t g_demag_uid = 0;
+
 struct mxb_demag {
     DemagPlan plan;
     cudaStream_t st = nullptr;
     cudaStream_t own = nullptr;
+    uint64_t uid = ++g_demag_uid;   // identity for cached CUDA graphs
     double* io[2] = {nullptr, nullptr};  // host-facing scratch (3N each)
 };
 
@@ -60,6 +65,12 @@ struct mxb_ctx {
     double* tB = nullptr;
     double* bias_dev = nullptr;   // (3,N) spatial bias scratch
     double* mri[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // F0..F2, R, V, K2, K3
+    // one captured step per (configuration, buffer parity): replayed by mxb_run
+    struct Graph {
+        std::vector<double> key;
+        cudaGraphExec_t exec;
+    };
+    std::vector<Graph> graphs;
     Ctl* ctl = nullptr;
     double* partials = nullptr;
     bool state_valid = false;
@@ -190,6 +201,7 @@ int mxb_ctx_destroy(mxb_ctx* c) {
     double* bufs[] = {c->mat_buf, c->Yb[0], c->Yb[1], c->P, c->K1, c->S, c->Hd, c->tA, c->tB, c->bias_dev, c->partials};
     for (double* b : bufs) if (b) cudaFree(b);
     for (double* b : c->mri) if (b) cudaFree(b);
+    for (auto& gr : c->graphs) cudaGraphExecDestroy(gr.exec);
     if (c->ctl) cudaFree(c->ctl);
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -852,7 +864,40 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
             if ((rc = ensure(&c->mri[i], fbytes(c->g)))) return rc;
     }
     int row_i = 0;
+    // constant bias: replay one captured CUDA graph per step (launch-bound small
+    // grids); the first step of a configuration runs eagerly (attribute setup)
+    static const bool graphs_on = getenv("MXB_GRAPHS") == nullptr || atoi(getenv("MXB_GRAPHS")) != 0;
+    const bool use_graph = graphs_on && !ra->stage_bias;
     for (int64_t k = 0; k < ra->nsteps; ++k) {
+        if (use_graph && k > 0) {
+            std::vector<double> key = {(double)t->mask, (double)t->ghost_mode, (double)t->precession,
+                                       (double)t->damping, (double)ra->method, (double)ra->renorm_each_stage,
+                                       (double)c->exact, (double)c->cur, ra->dt, ra->theta,
+                                       a.bias[0], a.bias[1], a.bias[2], (double)(uintptr_t)a.bias_field,
+                                       (double)(d ? d->uid : 0), (double)ra->fast_mask};
+            cudaGraphExec_t ex = nullptr;
+            for (auto& gr : c->graphs)
+                if (gr.key == key) { ex = gr.exec; break; }
+            if (!ex) {
+                MXB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+                int crc = ra->method == MXB_MRI_KW3
+                              ? enqueue_step_mri(c, d, a, t->mask, ra->fast_mask & t->mask, ra->dt,
+                                                 ra->theta, nullptr, &row_i, ra->renorm_each_stage != 0)
+                              : enqueue_step(c, d, a, ra->method, ra->dt, nullptr,
+                                             ra->renorm_each_stage != 0, use_demag);
+                cudaGraph_t gr = nullptr;
+                cudaError_t e = cudaStreamEndCapture(c->st, &gr);
+                if (crc) { if (gr) cudaGraphDestroy(gr); return crc; }
+                if (e != cudaSuccess) return cuda_fail(e, "graph capture", __FILE__, __LINE__);
+                e = cudaGraphInstantiate(&ex, gr, 0);
+                cudaGraphDestroy(gr);
+                if (e != cudaSuccess) return cuda_fail(e, "graph instantiate", __FILE__, __LINE__);
+                c->graphs.push_back({key, ex});
+            }
+            MXB_CUDA(cudaGraphLaunch(ex, c->st));
+            c->cur ^= 1;
+            continue;
+        }
         if (ra->method == MXB_MRI_KW3) {
             rc = enqueue_step_mri(c, d, a, t->mask, ra->fast_mask & t->mask, ra->dt, ra->theta,
                                   ra->stage_bias, &row_i, ra->renorm_each_stage != 0);
