@@ -73,6 +73,7 @@ struct mxb_ctx {
     std::vector<Graph> graphs;
     Ctl* ctl = nullptr;
     double* partials = nullptr;
+    int last_nparts = 0;          // partials of the last mxb_stage_dev final stage
     bool state_valid = false;
 };
 
@@ -945,6 +946,7 @@ int mxb_stage_dev(mxb_ctx* c, int mode, const mxb_terms* t, const mxb_stage_io* 
     a.dt6 = io->dt6;
     a.halt = &c->ctl->halt;
     if ((t->mask & MXB_TERM_DEMAG) && !a.hd) { set_error("demag term without a demag field"); return MXB_EINVAL; }
+    if (mode == M_RK4 || mode == M_EULER) c->last_nparts = stage_nparts(a);
     return launch_stage(mode, c->exact, a, c->st, false);
 }
 
@@ -952,6 +954,7 @@ int mxb_step_partials_dev(mxb_ctx* c, double* out8) {
     if (!c || !out8) { set_error("null argument"); return MXB_EINVAL; }
     cudaSetDevice(c->dev);
     StageArgs a = base_args(c);
+    a.nparts = c->last_nparts;
     return launch_partials(a, out8, c->st);
 }
 

@@ -19,6 +19,8 @@
 #include <float.h>
 #include <limits.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "stencil.cuh"
@@ -38,7 +40,7 @@ __global__ void k_commit(Ctl* ctl, const double* totals8);
 
 // slab decomposition: local (sum m/Ms x3 | drift, halt, -dead) of the last final stage
 int launch_partials(const StageArgs& a, double* out8, cudaStream_t st) {
-    k_partials<<<1, 1024, 0, st>>>(a.ctl, a.partials, stage_blocks(a.g.N), out8);
+    k_partials<<<1, 1024, 0, st>>>(a.ctl, a.partials, a.nparts > 0 ? a.nparts : stage_blocks(a.g.N), out8);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
@@ -50,7 +52,8 @@ int launch_commit(const StageArgs& a, const double* totals8, cudaStream_t st) {
 }
 
 int launch_finalize(const StageArgs& a, int mode, cudaStream_t st) {
-    k_finalize<<<1, 1024, 0, st>>>(a.ctl, a.partials, stage_blocks(a.g.N), mode, a.halt);
+    k_finalize<<<1, 1024, 0, st>>>(a.ctl, a.partials, a.nparts > 0 ? a.nparts : stage_blocks(a.g.N),
+                                   mode, a.halt);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
@@ -251,6 +254,14 @@ __device__ __forceinline__ void bulk_neighbour(const StageArgs& a, const double*
     for (int q = 0; q < 3; ++q) nb[q] = m[q] + sd * (pr * cr[q]);
 }
 
+template <bool E, bool U>
+__device__ __forceinline__ void heff_nb(const StageArgs& a, const double* f, long long idx, int i,
+                                        int j, int k, const double m[3], const CellMat& cm,
+                                        uint32_t terms, const double xp[3], const double xm[3],
+                                        const double yp[3], const double ym[3], const double zp[3],
+                                        const double zm[3], double fxp, double fxm, double fyp,
+                                        double fym, double fzp, double fzm, double h[3]);
+
 // H_eff of one cell in the reference accumulation order.
 template <bool E, bool U>
 __device__ __forceinline__ void heff_cell(const StageArgs& a, const double* f, long long idx, int i,
@@ -278,6 +289,24 @@ __device__ __forceinline__ void heff_cell(const StageArgs& a, const double* f, l
         neighbour<E, U>(a, f, idx, k, g.nz, sz, +1, 2, m, cm, zp, fzp);
         neighbour<E, U>(a, f, idx, k, g.nz, sz, -1, 2, m, cm, zm, fzm);
     }
+    heff_nb<E, U>(a, f, idx, i, j, k, m, cm, terms, xp, xm, yp, ym, zp, zm, fxp, fxm, fyp, fym, fzp,
+                  fzm, h);
+}
+
+// H_eff from gathered neighbours (values after the ghost rules) and face
+// coefficients, in the reference accumulation order.
+template <bool E, bool U>
+__device__ __forceinline__ void heff_nb(const StageArgs& a, const double* f, long long idx, int i,
+                                        int j, int k, const double m[3], const CellMat& cm,
+                                        uint32_t terms, const double xp[3], const double xm[3],
+                                        const double yp[3], const double ym[3], const double zp[3],
+                                        const double zm[3], double fxp, double fxm, double fyp,
+                                        double fym, double fzp, double fzm, double h[3]) {
+    const Grid& g = a.g;
+    h[0] = 0.0; h[1] = 0.0; h[2] = 0.0;
+    const bool ex = terms & MXB_TERM_EXCHANGE;
+    const bool dmi = terms & MXB_TERM_DMI;
+    const long long sy = g.nx, sz = (long long)g.nx * g.ny;
     if (ex) {
         double acc[3] = {0.0, 0.0, 0.0};
         if (g.nx > 1) {
@@ -465,6 +494,64 @@ __device__ void reduce_partials(const double* partials, int nblk, const bool is_
     for (int q = 0; q < NV; ++q) out[q] = v[q];
 }
 
+// torque and the integrator stage of one cell given its H_eff (writes outputs,
+// accumulates the step partials for the final RK4 / Euler stage)
+template <int MODE, bool E>
+__device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, const CellMat& cm,
+                                           const double m[3], const double h[3], double red[4]) {
+    const long long N = a.g.N;
+    constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
+        if (MODE == M_HEFF) {
+        a.out[idx] = h[0]; a.out[N + idx] = h[1]; a.out[2 * N + idx] = h[2];
+    } else {
+        double kk[3];
+        torque<E>(m, h, cm, a.prec, a.damp, kk);
+        if (MODE == M_RHS) {
+            a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
+        } else {
+            const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
+            double v[3];
+            if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) v[q] = add<E>(y[q], mul<E>(a.c, kk[q]));
+                if (MODE == M_RK1) {
+                    a.k1_out[idx] = kk[0]; a.k1_out[N + idx] = kk[1]; a.k1_out[2 * N + idx] = kk[2];
+                } else if (MODE == M_RK2) {
+                    a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
+                } else if (MODE == M_RK3) {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
+                }
+            } else {  // M_RK4
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
+                    v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
+                }
+            }
+            if (kFinal) {
+                if (cm.mag) {
+                    const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
+                    double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
+                    if (!(d == d) || isinf(d)) d = DBL_MAX;  // non-finite drift (llg.py:351)
+                    red[3] = fmax(red[3], d);
+                }
+                // a dead cell here always has drift 1 > 0.1, so the blow-up wins
+                // (llg.py:348-355); only record it, never halt mid-kernel
+                if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
+                if (cm.mag) {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+                        red[q] += E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms);
+                }
+            } else if (a.renorm) {
+                if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
+            }
+            a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // the fused stage kernel
 // ---------------------------------------------------------------------------
@@ -486,55 +573,7 @@ __global__ void __launch_bounds__(256, 3) k_stage(StageArgs a) {
         const double m[3] = {ld(a.ys, idx), ld(a.ys, N + idx), ld(a.ys, 2 * N + idx)};
         double h[3];
         heff_cell<E, U>(a, a.ys, idx, i, j, k, m, cm, a.terms, h);
-        if (MODE == M_HEFF) {
-            a.out[idx] = h[0]; a.out[N + idx] = h[1]; a.out[2 * N + idx] = h[2];
-        } else {
-            double kk[3];
-            torque<E>(m, h, cm, a.prec, a.damp, kk);
-            if (MODE == M_RHS) {
-                a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
-            } else {
-                const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
-                double v[3];
-                if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) v[q] = add<E>(y[q], mul<E>(a.c, kk[q]));
-                    if (MODE == M_RK1) {
-                        a.k1_out[idx] = kk[0]; a.k1_out[N + idx] = kk[1]; a.k1_out[2 * N + idx] = kk[2];
-                    } else if (MODE == M_RK2) {
-                        a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
-                    } else if (MODE == M_RK3) {
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
-                    }
-                } else {  // M_RK4
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
-                        v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
-                    }
-                }
-                if (kFinal) {
-                    if (cm.mag) {
-                        const double n2 = add<E>(add<E>(mul<E>(v[0], v[0]), mul<E>(v[1], v[1])), mul<E>(v[2], v[2]));
-                        double d = fabs(sub<E>(E ? div_rn(sqrt(n2), cm.Ms) : sqrt(n2) * (1.0 / cm.Ms), 1.0));
-                        if (!(d == d) || isinf(d)) d = DBL_MAX;  // non-finite drift (llg.py:351)
-                        red[3] = d;
-                    }
-                    // a dead cell here always has drift 1 > 0.1, so the blow-up wins
-                    // (llg.py:348-355); only record it, never halt mid-kernel
-                    if (!renorm_cell<E>(v, cm)) atomicMin((long long*)&a.ctl->dead_flat, idx);
-                    if (cm.mag) {
-#pragma unroll
-                        for (int q = 0; q < 3; ++q)
-                            red[q] = E ? div_rn(v[q], cm.Ms) : v[q] * (1.0 / cm.Ms);
-                    }
-                } else if (a.renorm) {
-                    if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
-                }
-                a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
-            }
-        }
+        stage_tail<MODE, E>(a, idx, cm, m, h, red);
     }
     if (kFinal) {
         const bool is_max[4] = {false, false, false, true};
@@ -642,6 +681,147 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
     if (c->eq_tol >= 0.0 && res < c->eq_tol) c->halt = MXB_EQUILIBRATED;
 }
 
+// ---------------------------------------------------------------------------
+// z-marching variant for uniform, fully magnetic materials: a CTA owns a
+// 32 x 8 column tile and walks ZC planes; x/y neighbours come from a shared
+// tile with a one-cell halo ring, z neighbours stay in registers.  Same
+// neighbour values, face coefficients and arithmetic as k_stage.
+// ---------------------------------------------------------------------------
+constexpr int ZTX = 32, ZTY = 8, ZC = 16;
+
+template <bool E>
+__device__ __forceinline__ void ghost_nb(const StageArgs& a, int axis, int step, const double m[3],
+                                         double p, double nb[3]) {
+    if (a.ghost == MXB_GHOST_NEUMANN || axis == 2) {
+        nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];
+        return;
+    }
+    const double d = axis == 0 ? a.g.dx : a.g.dy;
+    const double sd = step > 0 ? d : -d;
+    if (axis == 0) {
+        nb[0] = add<E>(m[0], mul<E>(sd, mul<E>(p, m[2])));
+        nb[1] = add<E>(m[1], mul<E>(sd, 0.0));
+        nb[2] = add<E>(m[2], mul<E>(sd, mul<E>(-p, m[0])));
+    } else {
+        nb[0] = add<E>(m[0], mul<E>(sd, 0.0));
+        nb[1] = add<E>(m[1], mul<E>(sd, mul<E>(p, m[2])));
+        nb[2] = add<E>(m[2], mul<E>(sd, mul<E>(-p, m[1])));
+    }
+}
+
+template <int MODE, bool E>
+__global__ void __launch_bounds__(256, 3) k_stage_zm(StageArgs a) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
+    __shared__ double tile[3][ZTY + 2][ZTX + 2];
+    const Grid& g = a.g;
+    const long long N = g.N, plane = (long long)g.nx * g.ny;
+    const int tx = threadIdx.x & (ZTX - 1), ty = threadIdx.x / ZTX;
+    const int i = blockIdx.x * ZTX + tx, j = blockIdx.y * ZTY + ty;
+    const int k0 = blockIdx.z * ZC, k1 = min(k0 + ZC, g.nz);
+    const bool in = i < g.nx && j < g.ny;
+    const long long col = (long long)j * g.nx + i;
+    const CellMat cm = cell_mat<E, true>(a, 0);
+    const double* f = a.ys;
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    auto load = [&](int k, double v[3]) -> bool {
+        if (!in) return false;
+        if (k >= 0 && k < g.nz) {
+            const long long o = (long long)k * plane + col;
+            v[0] = ld(f, o); v[1] = ld(f, N + o); v[2] = ld(f, 2 * N + o);
+            return true;
+        }
+        const double* hp = k < 0 ? a.halo_lo : a.halo_hi;
+        if (!hp) return false;
+        v[0] = ld(hp, col); v[1] = ld(hp, plane + col); v[2] = ld(hp, 2 * plane + col);
+        return true;
+    };
+    double zmv[3] = {0, 0, 0}, zcv[3] = {0, 0, 0}, zpv[3] = {0, 0, 0};
+    load(k0, zcv);
+    bool zm_ok = load(k0 - 1, zmv);
+    const bool ex = a.terms & MXB_TERM_EXCHANGE;
+    for (int k = k0; k < k1; ++k) {
+        const bool zp_ok = load(k + 1, zpv);
+        __syncthreads();
+        if (in) {
+            const long long o = (long long)k * plane + col;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                tile[q][ty + 1][tx + 1] = zcv[q];
+                if (tx == 0 && i > 0) tile[q][ty + 1][0] = ld(f, q * N + o - 1);
+                if (tx == ZTX - 1 && i + 1 < g.nx) tile[q][ty + 1][ZTX + 1] = ld(f, q * N + o + 1);
+                if (ty == 0 && j > 0) tile[q][0][tx + 1] = ld(f, q * N + o - g.nx);
+                if (ty == ZTY - 1 && j + 1 < g.ny) tile[q][ZTY + 1][tx + 1] = ld(f, q * N + o + g.nx);
+            }
+        }
+        __syncthreads();
+        if (in) {
+            const long long idx = (long long)k * plane + col;
+            const double m[3] = {zcv[0], zcv[1], zcv[2]};
+            double xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
+            const double hf = a.dv.face, A = cm.A, p = cm.slope_p;
+            const bool okxp = i + 1 < g.nx, okxm = i > 0, okyp = j + 1 < g.ny, okym = j > 0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                xp[q] = tile[q][ty + 1][tx + 2];
+                xm[q] = tile[q][ty + 1][tx];
+                yp[q] = tile[q][ty + 2][tx + 1];
+                ym[q] = tile[q][ty][tx + 1];
+                zp[q] = zpv[q];
+                zm[q] = zmv[q];
+            }
+            if (!okxp) ghost_nb<E>(a, 0, +1, m, p, xp);
+            if (!okxm) ghost_nb<E>(a, 0, -1, m, p, xm);
+            if (!okyp) ghost_nb<E>(a, 1, +1, m, p, yp);
+            if (!okym) ghost_nb<E>(a, 1, -1, m, p, ym);
+            if (!zp_ok) ghost_nb<E>(a, 2, +1, m, p, zp);
+            if (!zm_ok) ghost_nb<E>(a, 2, -1, m, p, zm);
+            double h[3];
+            (void)ex;
+            heff_nb<E, true>(a, f, idx, i, j, k, m, cm, a.terms, xp, xm, yp, ym, zp, zm,
+                             okxp ? hf : A, okxm ? hf : A, okyp ? hf : A, okym ? hf : A,
+                             zp_ok ? hf : A, zm_ok ? hf : A, h);
+            stage_tail<MODE, E>(a, idx, cm, m, h, red);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { zmv[q] = zcv[q]; zcv[q] = zpv[q]; }
+        zm_ok = true;
+    }
+    if (kFinal) {
+        const bool is_max[4] = {false, false, false, true};
+        block_reduce<4>(red, is_max);
+        if (threadIdx.x == 0) {
+            const long long b = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            double* pp = a.partials + b * kReduceSlots;
+            pp[0] = red[0]; pp[1] = red[1]; pp[2] = red[2]; pp[3] = red[3];
+        }
+    }
+}
+
+static bool zm_eligible(const StageArgs& a) {
+    static const bool on = getenv("MXB_ZMARCH") == nullptr || atoi(getenv("MXB_ZMARCH")) != 0;
+    return on && a.mat.uniform && a.mat.all_magnetic && a.ghost != MXB_GHOST_PERIODIC &&
+           !(a.terms & (MXB_TERM_CUBIC | MXB_TERM_BULK_DMI)) && (long long)a.g.nx * a.g.ny >= 256;
+}
+
+static dim3 zm_grid(const Grid& g) {
+    return dim3((g.nx + ZTX - 1) / ZTX, (g.ny + ZTY - 1) / ZTY, (g.nz + ZC - 1) / ZC);
+}
+
+int stage_nparts(const StageArgs& a) {
+    if (zm_eligible(a)) {
+        const dim3 gz = zm_grid(a.g);
+        return (int)(gz.x * gz.y * gz.z);
+    }
+    return stage_blocks(a.g.N);
+}
+
+template <int MODE>
+static void launch_zm(bool exact, const StageArgs& a, cudaStream_t st) {
+    if (exact) k_stage_zm<MODE, true><<<zm_grid(a.g), kBlock, 0, st>>>(a);
+    else k_stage_zm<MODE, false><<<zm_grid(a.g), kBlock, 0, st>>>(a);
+}
+
 template <int MODE, bool E>
 static void launch_mode_u(const StageArgs& a, cudaStream_t st, int nb) {
     if (a.mat.uniform) k_stage<MODE, E, true><<<nb, kBlock, 0, st>>>(a);
@@ -654,8 +834,27 @@ static void launch_mode(bool exact, const StageArgs& a, cudaStream_t st, int nb)
     else launch_mode_u<MODE, false>(a, st, nb);
 }
 
-int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st, bool finalize) {
+int launch_stage(int mode, bool exact, const StageArgs& a0, cudaStream_t st, bool finalize) {
+    StageArgs a = a0;
     const int nb = stage_blocks(a.g.N);
+    if (zm_eligible(a)) {
+        const dim3 gz = zm_grid(a.g);
+        a.nparts = (int)(gz.x * gz.y * gz.z);
+        switch (mode) {
+            case M_HEFF: launch_zm<M_HEFF>(exact, a, st); break;
+            case M_RHS: launch_zm<M_RHS>(exact, a, st); break;
+            case M_RK1: launch_zm<M_RK1>(exact, a, st); break;
+            case M_RK2: launch_zm<M_RK2>(exact, a, st); break;
+            case M_RK3: launch_zm<M_RK3>(exact, a, st); break;
+            case M_RK4: launch_zm<M_RK4>(exact, a, st); break;
+            case M_EULER: launch_zm<M_EULER>(exact, a, st); break;
+            default: set_error("bad stage mode"); return MXB_EINVAL;
+        }
+        MXB_LAUNCH_CHECK();
+        if (finalize && (mode == M_RK4 || mode == M_EULER)) return launch_finalize(a, 0, st);
+        return MXB_OK;
+    }
+    a.nparts = nb;
     switch (mode) {
         case M_HEFF: launch_mode<M_HEFF>(exact, a, st, nb); break;
         case M_RHS: launch_mode<M_RHS>(exact, a, st, nb); break;

@@ -62,6 +62,7 @@ struct StageArgs {
     const double* hms_hi;
     const double* hA_lo;
     const double* hA_hi;
+    int nparts;             // block partials written by the last final-stage kernel (0: one per 256 cells)
 };
 
 int launch_stage(int mode, bool exact, const StageArgs& a, cudaStream_t st, bool finalize = true);
@@ -84,6 +85,7 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
                     cudaStream_t st);
 int stage_blocks(long long N);
 int launch_finalize(const StageArgs& a, int mode, cudaStream_t st);
+int stage_nparts(const StageArgs& a);   // block partials a final-stage launch with these args writes
 int launch_partials(const StageArgs& a, double* out8, cudaStream_t st);
 int launch_commit(const StageArgs& a, const double* totals8, cudaStream_t st);
 Derived derive(const MatDev& m, const Grid& g);
