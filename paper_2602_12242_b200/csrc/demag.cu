@@ -11,6 +11,7 @@
 // A thin film (nz = 1) fuses the y transform with the multiply instead.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -344,10 +345,32 @@ int DemagPlan::init(const mxb_grid& gr, int device, int nranks, int rk) {
     MXB_CUDA(cudaMalloc(&XS, xs * sizeof(double2)));
     if (G > 1) MXB_CUDA(cudaMalloc(&XR, xs * sizeof(double2)));
     else XR = XS;
-    if (pz > 1 && py > 1) MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
-    else X2 = XR;
-    bytes = (xs * (G > 1 ? 2 : 1) + (X2 != XR ? x2 : 0)) * sizeof(double2);
+    bytes = xs * (G > 1 ? 2 : 1) * sizeof(double2);
+    // the y/z intermediate of the 5-pass layout; a plane-pipeline candidate
+    // allocates it only if finish_spectra does not select the pipeline
+    if (pz > 1 && py > 1) {
+        if (!pipe_candidate()) {
+            MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
+            bytes += x2 * sizeof(double2);
+        }
+    } else {
+        X2 = XR;
+    }
     return MXB_OK;
+}
+
+// shapes the plane pipeline covers (single rank, 3-D, ny == nz, power-of-two
+// padding, fast x rows); MXB_PIPE=0 disables it, MXB_PIPE=1 lifts the size floor
+bool DemagPlan::pipe_candidate() const {
+    if (G != 1 || pz <= 1 || py <= 1 || !fast) return false;
+    if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
+    if (!pipe_shape_ok(g.ny, g.nz)) return false;
+    const char* e = getenv("MXB_PIPE");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    // measured on B200: on par with the 5-pass path at L = 1024 (and 13 GB less
+    // HBM at 512^3), slower below; see DESIGN.md
+    return pz >= 1024;
 }
 
 void DemagPlan::release() {
@@ -355,6 +378,12 @@ void DemagPlan::release() {
     for (auto& t : tw) if (t) cudaFree(t);
     if (twm) cudaFree(twm);
     if (Kq) cudaFree(Kq);
+    if (Kp) cudaFree(Kp);
+    if (slots) cudaFree(slots);
+    if (bar) cudaFree(bar);
+    Kp = nullptr;
+    slots = nullptr;
+    bar = nullptr;
     if (Kc && Kc != K) cudaFree(Kc);
     if (K) cudaFree(K);
     if (X2 && X2 != XR) cudaFree(X2);
@@ -446,6 +475,42 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
     if (Kc && Kc != K) { cudaFree(Kc); }
     Kc = nullptr;
     kmode = 0;
+    pipe = false;
+    if (Kp) { cudaFree(Kp); Kp = nullptr; }
+    if (slots) { cudaFree(slots); slots = nullptr; }
+    if (bar) { cudaFree(bar); bar = nullptr; }
+    if (G == 1) {   // standard row layout unless the pipeline is selected below
+        CH = hx;
+        CHP = hxp;
+        blk = (long long)nz_l * g.ny * CHP * 3;
+    }
+    if (symmetric && pipe_candidate()) {
+        // plane-major quarter spectra, slot ring, barrier; x passes switch to [kx][z][y][3]
+        const int L2 = pz / 2 + 1;
+        const size_t nk = (size_t)hx * L2 * L2 * 6;
+        const size_t ns = (size_t)3 * g.nz * py * 3;
+        MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
+        MXB_CUDA(cudaMalloc(&slots, ns * sizeof(double2)));
+        MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx) * sizeof(unsigned)));
+        int rc = pipe_quarter(K, Kp, pz, hx, hxp, st);
+        if (rc) return rc;
+        CH = 1;
+        CHP = 1;
+        blk = (long long)g.nz * g.ny * 3;
+        kmode = 3;
+        pipe = true;
+        MXB_CUDA(cudaStreamSynchronize(st));
+        cudaFree(K);
+        K = nullptr;
+        bytes += nk * sizeof(double) + ns * sizeof(double2);
+        has_kernel = true;
+        return MXB_OK;
+    }
+    if (pz > 1 && py > 1 && !X2) {
+        const size_t x2 = (size_t)g.nz * py * CHP * 3;
+        MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
+        bytes += x2 * sizeof(double2);
+    }
     if (symmetric && fast_fused_ok(L)) {
         const int e_is_z = pz > 1 ? 1 : (py > 1 ? 0 : 1);
         const size_t n = (size_t)(L / 2 + 1) * (GG / 2 + 1) * CHP * 6;
@@ -510,6 +575,13 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
     const long long row = (long long)CHP * 3;   // complex elements per (z,y) row of the chunk
     int rc;
     if (kxn <= 0) { mark(2); mark(3); mark(4); return MXB_OK; }
+    if (pipe) {
+        mark(2);
+        rc = pipe_yz(XR, slots, Kp, bar, hx, nz, scale, plz.tw, st, halt);
+        mark(3);
+        mark(4);
+        return rc;
+    }
     auto cols = [&](int dir, const double2* in, double2* out, int n_in, int n_out, long long OS_in,
                     long long OS_out) {
         int r = -1;
@@ -554,12 +626,21 @@ int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int*
                          cudaEvent_t* ev) {
     if (G != 1) { set_error("field_dev is the single-rank pipeline"); return MXB_EINVAL; }
     if (!has_kernel) { set_error("demag kernel has no spectra (call set_packed or build)"); return MXB_EINVAL; }
+    // MXB_SYNC_DEBUG=1: synchronise after every pass and name the one that failed
+    static const bool dbg = getenv("MXB_SYNC_DEBUG") != nullptr;
+    auto sync = [&](const char* what) -> int {
+        if (!dbg) return MXB_OK;
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, what, __FILE__, __LINE__);
+        return MXB_OK;
+    };
     if (ev) cudaEventRecord(ev[0], st);
     int rc = x_forward(m, st, halt);
-    if (rc) return rc;
+    if (rc || (rc = sync("x_forward"))) return rc;
     if (ev) cudaEventRecord(ev[1], st);
-    if ((rc = yz(st, halt, ev))) return rc;
+    if ((rc = yz(st, halt, ev)) || (rc = sync("yz"))) return rc;
     rc = x_inverse(h, st, halt);
+    if (!rc) rc = sync("x_inverse");
     if (ev) cudaEventRecord(ev[5], st);
     return rc;
 }

@@ -28,6 +28,12 @@ int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
               int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
               const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt);
 
+// L2-resident y/z pipeline over kx planes (yz_pipe.cu)
+bool pipe_shape_ok(int ny, int nz);
+int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
+            const double2* tw, cudaStream_t st, const int* halt);
+int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st);
+
 struct DemagPlan {
     int dev = 0;
     Grid g{};                // GLOBAL grid
@@ -46,7 +52,12 @@ struct DemagPlan {
     double2* K = nullptr;    // full spectra [pz][py][hxp][6] complex (build scratch)
     double2* Kc = nullptr;   // complex spectra of the chunk [pz][py][CHP][6]
     double* Kq = nullptr;    // parity-reduced real spectra of the chunk [L/2+1][G/2+1][CHP][6]
-    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq
+    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp
+    // plane pipeline (kmode 3): XS is plane-major [kx][z][y][3] (CH = CHP = 1)
+    bool pipe = false;
+    double* Kp = nullptr;     // [hx][py/2+1][pz/2+1][6]
+    double2* slots = nullptr; // 3 x [nz][py][3]
+    unsigned* bar = nullptr;
     Plan1D plm{};            // length px/2 (fast x rows)
     double2* twm = nullptr;
     bool fast = true;        // use the register-resident kernels where shapes allow
@@ -56,6 +67,7 @@ struct DemagPlan {
     int fused_G() const { return pz > 1 ? py : 1; }
 
     int init(const mxb_grid& g, int device, int nranks = 1, int rank = 0);
+    bool pipe_candidate() const;
     void release();
     int spectra_from_packed_dev(const double* P, cudaStream_t st);
     int spectra_x_component(const double* Pc, int c, cudaStream_t st);
