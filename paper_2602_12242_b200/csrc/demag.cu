@@ -491,7 +491,7 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         const size_t ns = (size_t)3 * g.nz * py * 3;
         MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
         MXB_CUDA(cudaMalloc(&slots, ns * sizeof(double2)));
-        MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx) * sizeof(unsigned)));
+        MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx + 3 * (size_t)g.nz) * sizeof(unsigned)));
         int rc = pipe_quarter(K, Kp, pz, hx, hxp, st);
         if (rc) return rc;
         CH = 1;

@@ -1,0 +1,113 @@
+// Warp-per-line FFT of length 1024 = 32 x 32 (four-step), for the fast path.
+//
+// A whole line lives in one warp: lane l holds the 32 points x[l + 32 m].
+//   1. a 32-point DFT over m in registers (4 x 8 split, constant twiddles)
+//   2. twiddle by w1024^(l k) from the exact table
+//   3. one transpose through a warp-private 16 KB shared tile (XOR swizzle,
+//      bank-conflict free both ways, __syncwarp only)
+//   4. a 32-point DFT over l in registers
+// Output: lane j holds X[j + 32 k] in register p(k) = 8 (k % 4) + k / 4.
+// Compared with the CTA-wide radix-16 Stockham core (fft_fast.cuh) this is
+// one shared-memory exchange instead of two and no CTA barrier; zero-padded
+// inputs and unneeded outputs fold away at compile time (registers that are
+// constant zero / never stored).
+#pragma once
+
+#include "fft_generic.cuh"
+
+namespace mxb {
+namespace fw {
+
+// a * exp(DIR * 2 pi i e / 32); e is a compile-time constant after unrolling
+template <int DIR> __device__ __forceinline__ double2 w32(double2 a, int e) {
+    e &= 31;
+    if (e == 0) return a;
+    if (e == 8) return mul_mi<DIR>(a);
+    if (e == 16) return make_double2(-a.x, -a.y);
+    if (e == 24) return mul_mi<-DIR>(a);
+    double c, s;
+    switch (e) {
+        case 0: c = 1.000000000000000000000000; s = 0.0; break;
+        case 1: c = 0.9807852804032304491261822; s = 0.1950903220161282678482849; break;
+        case 2: c = 0.9238795325112867561281832; s = 0.3826834323650897717284600; break;
+        case 3: c = 0.8314696123025452370787884; s = 0.5555702330196022247428308; break;
+        case 4: c = 0.7071067811865475244008444; s = 0.7071067811865475244008444; break;
+        case 5: c = 0.5555702330196022247428308; s = 0.8314696123025452370787884; break;
+        case 6: c = 0.3826834323650897717284600; s = 0.9238795325112867561281832; break;
+        case 7: c = 0.1950903220161282678482849; s = 0.9807852804032304491261822; break;
+        case 8: c = 2.067032109826398823649690e-43; s = 1.000000000000000000000000; break;
+        case 9: c = -0.1950903220161282678482849; s = 0.9807852804032304491261822; break;
+        case 10: c = -0.3826834323650897717284600; s = 0.9238795325112867561281832; break;
+        case 11: c = -0.5555702330196022247428308; s = 0.8314696123025452370787884; break;
+        case 12: c = -0.7071067811865475244008444; s = 0.7071067811865475244008444; break;
+        case 13: c = -0.8314696123025452370787884; s = 0.5555702330196022247428308; break;
+        case 14: c = -0.9238795325112867561281832; s = 0.3826834323650897717284600; break;
+        case 15: c = -0.9807852804032304491261822; s = 0.1950903220161282678482849; break;
+        case 16: c = -1.000000000000000000000000; s = 4.134064219652797647299381e-43; break;
+        case 17: c = -0.9807852804032304491261822; s = -0.1950903220161282678482849; break;
+        case 18: c = -0.9238795325112867561281832; s = -0.3826834323650897717284600; break;
+        case 19: c = -0.8314696123025452370787884; s = -0.5555702330196022247428308; break;
+        case 20: c = -0.7071067811865475244008444; s = -0.7071067811865475244008444; break;
+        case 21: c = -0.5555702330196022247428308; s = -0.8314696123025452370787884; break;
+        case 22: c = -0.3826834323650897717284600; s = -0.9238795325112867561281832; break;
+        case 23: c = -0.1950903220161282678482849; s = -0.9807852804032304491261822; break;
+        case 24: c = 2.233876440654988324291948e-41; s = -1.000000000000000000000000; break;
+        case 25: c = 0.1950903220161282678482849; s = -0.9807852804032304491261822; break;
+        case 26: c = 0.3826834323650897717284600; s = -0.9238795325112867561281832; break;
+        case 27: c = 0.5555702330196022247428308; s = -0.8314696123025452370787884; break;
+        case 28: c = 0.7071067811865475244008444; s = -0.7071067811865475244008444; break;
+        case 29: c = 0.8314696123025452370787884; s = -0.5555702330196022247428308; break;
+        case 30: c = 0.9238795325112867561281832; s = -0.3826834323650897717284600; break;
+        case 31: c = 0.9807852804032304491261822; s = -0.1950903220161282678482849; break;
+        default: c = 1.0; s = 0.0;
+    }
+    if (DIR < 0) s = -s;
+    return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+
+// in place; v[8 k1 + k2] = X[k1 + 4 k2] on exit (input natural order)
+template <int DIR> __device__ __forceinline__ void dft32(double2 (&v)[32]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) {
+        double2 q[4] = {v[n2], v[8 + n2], v[16 + n2], v[24 + n2]};
+        dft4<DIR>(q);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[8 * k1 + n2] = w32<DIR>(q[k1], n2 * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft8<DIR>(&v[8 * k1]);
+}
+
+__host__ __device__ constexpr int p32(int k) { return 8 * (k % 4) + k / 4; }
+
+// transpose tile: row r (the step-1 frequency), column l (the lane)
+__device__ __forceinline__ int tsw(int r, int l) { return r * 32 + (l ^ (r & 7)); }
+
+// v[m] = x[lane + 32 m] on entry; lane j holds X[j + 32 k] in v[p32(k)] on exit.
+// W: this warp's 1024-element tile (free on entry, clobbered).
+template <int DIR>
+__device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane, const double2* __restrict__ tw) {
+    dft32<DIR>(v);
+    __syncwarp();
+    // w1024^(lane k) as a running product, re-anchored from the exact table
+    // every 8 steps (<= 7 products; loading all 31 would pin ~120 registers)
+    const double2 w1 = twid<DIR>(tw, lane);
+    double2 w = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        if (k & 7) w = k == 1 ? w1 : cmul(w, w1);
+        else if (k) w = twid<DIR>(tw, lane * k);
+        const double2 a = k ? cmul(v[p32(k)], w) : v[p32(k)];
+        W[tsw(k, lane)] = a;
+        // keep the chain in step with the stores: computed ahead, all 31
+        // twiddles would stay live across the first DFT
+        asm volatile("" : "+d"(w.x), "+d"(w.y)::"memory");
+    }
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < 32; ++l) v[l] = W[tsw(lane, l)];
+    dft32<DIR>(v);
+}
+
+}  // namespace fw
+}  // namespace mxb

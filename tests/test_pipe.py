@@ -57,3 +57,21 @@ def test_pipeline_rk4_run_bitwise():
                       energy_in_samples=False).run_until(mx.StopCondition(max_steps=6))
         out.append(st.m.data.copy())
     assert np.array_equal(out[0], out[1])
+
+
+def test_warp_fft_pipeline_matches_five_pass():
+    """Opt-in warp-per-line FFT variant (fft_warp.cuh, L = 1024): different
+    rounding from the radix-16 path, so a normwise tolerance."""
+    g = mx.GridSpec(8, 512, 512, 2e-9, 2.5e-9, 3e-9)
+    m = np.random.default_rng(12).normal(size=(3,) + g.shape) * 8e5
+    h5 = build(g, False).field(m)
+    old = os.environ.get("MXB_PIPE_WARP")
+    os.environ["MXB_PIPE_WARP"] = "1"
+    try:
+        hw = build(g, True).field(m)
+    finally:
+        if old is None:
+            del os.environ["MXB_PIPE_WARP"]
+        else:
+            os.environ["MXB_PIPE_WARP"] = old
+    assert np.linalg.norm(hw - h5) <= 1e-13 * np.linalg.norm(h5)
