@@ -262,6 +262,30 @@ int mxb_time_demag_cufft(mxb_demag* d, int iters, double* ms_eval);
 int mxb_host_alloc(size_t bytes, void** p);
 int mxb_host_free(void* p);
 
+
+/* ---- FNO demag surrogate (fno.py:228-447): thin film, channels-first (3, ny, nx) ----
+ * params (float64), in this order:
+ *   lift.weight (width,3), lift.bias (width),
+ *   for k = 0..3: block{k}.spectral.pos (width,width,m1,m2) complex as (re,im) pairs,
+ *                 block{k}.spectral.neg (same), block{k}.local.weight (width,width),
+ *                 block{k}.local.bias (width),
+ *   proj.weight (3,width), proj.bias (3), norm.in_mean, norm.in_std, norm.out_mean,
+ *   norm.out_std (3 each).
+ * activation: 0 GELU (erf form), 1 ReLU.  Replaces FnoModel.infer (fno.py:372-394) and
+ * FnoDemag.field (fno.py:445-447). */
+typedef struct mxb_fno mxb_fno;
+int mxb_fno_create(int device, int width, int m1, int m2, int ny, int nx, int activation,
+                   const double* params, mxb_fno** out);
+void mxb_fno_destroy(mxb_fno* f);
+/* host (3, ny, nx) -> host (3, ny, nx) */
+int mxb_fno_infer(mxb_fno* f, const double* x, double* y);
+/* device pointers, on the model's stream (synchronise before reading y) */
+int mxb_fno_infer_dev(mxb_fno* f, const double* x, double* y);
+/* spectral_conv (fno.py:228-255) of host (channels, ny, nx); w_pos/w_neg
+ * (channels, channels, m1, m2) complex as (re, im) pairs */
+int mxb_fno_spectral_conv(int device, int channels, int ny, int nx, int m1, int m2,
+                          const double* w_pos, const double* w_neg, const double* x, double* y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,13 @@ SIGNATURES = {
     "mxb_time_demag_cufft": ([C.c_void_p, C.c_int, _dp], C.c_int),
     "mxb_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], C.c_int),
     "mxb_host_free": ([C.c_void_p], C.c_int),
+    "mxb_fno_create": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp,
+                        C.POINTER(C.c_void_p)], C.c_int),
+    "mxb_fno_destroy": ([C.c_void_p], None),
+    "mxb_fno_infer": ([C.c_void_p, _dp, _dp], C.c_int),
+    "mxb_fno_infer_dev": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_fno_spectral_conv": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp],
+                              C.c_int),
 }
 
 _lock = threading.Lock()
