@@ -302,10 +302,17 @@ def main():
     hbm, which = peaks()
     pb = demag_bytes(g, kern)
     stencil_bytes = 504 * N               # per RK4 step (4 fused stage kernels)
-    kernels = [("x_r2c", pb[0], passes[0]), ("y_fwd", pb[1], passes[1]),
-               ("z_fused_mul", pb[2], passes[2]), ("y_inv", pb[3], passes[3]),
-               ("x_c2r", pb[4], passes[4]),
-               ("stage_stencil_llg", stencil_bytes / 4, ms_st.value / args.steps / 4)]
+    if kern.pipeline:
+        # one persistent kernel replaces the y forward, z fused and y inverse passes;
+        # its algorithmic bytes are theirs (SURVEY 8d fixed formulas)
+        kernels = [("x_r2c", pb[0], passes[0]),
+                   ("yz_plane_pipeline", pb[1] + pb[2] + pb[3], passes[1] + passes[2] + passes[3]),
+                   ("x_c2r", pb[4], passes[4])]
+    else:
+        kernels = [("x_r2c", pb[0], passes[0]), ("y_fwd", pb[1], passes[1]),
+                   ("z_fused_mul", pb[2], passes[2]), ("y_inv", pb[3], passes[3]),
+                   ("x_c2r", pb[4], passes[4])]
+    kernels.append(("stage_stencil_llg", stencil_bytes / 4, ms_st.value / args.steps / 4))
     share = {k: 4 * t for k, _, t in kernels}
     dom = max(kernels, key=lambda x: x[2])
     ach = dom[1] / (dom[2] * 1e-3) / 1e9

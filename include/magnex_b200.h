@@ -136,6 +136,9 @@ int mxb_demag_field_dev(mxb_demag* d, const double* m_dev, double* h_dev);
 size_t mxb_demag_bytes(mxb_demag* d);
 /* select the register-resident radix-16 kernels (1, default) or the generic
  * mixed-radix shared-memory kernels (0) where both cover the shape */
+/* spectra storage / y-z path of a built kernel: 0 complex (5-pass), 2 parity-reduced
+ * real (5-pass), 3 plane-major real + L2-resident y/z plane pipeline (yz_pipe.cu) */
+int mxb_demag_kmode(mxb_demag* d, int* kmode);
 int mxb_demag_set_fast(mxb_demag* d, int fast);
 
 /* ---- local operators and assembly (host buffers) ----------------------- */

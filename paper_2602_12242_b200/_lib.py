@@ -86,6 +86,7 @@ SIGNATURES = {
     "mxb_demag_field_dev": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "mxb_demag_bytes": ([C.c_void_p], C.c_size_t),
     "mxb_demag_set_fast": ([C.c_void_p, C.c_int], C.c_int),
+    "mxb_demag_kmode": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "mxb_term_field": ([C.c_void_p, C.c_uint32, C.c_int, _dp, _dp], C.c_int),
     "mxb_heff": ([C.c_void_p, C.c_void_p, C.POINTER(Terms), C.POINTER(Bias), _dp, _dp], C.c_int),
     "mxb_llg_rhs": ([C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp], C.c_int),

@@ -436,6 +436,12 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     return MXB_OK;
 }
 
+int mxb_demag_kmode(mxb_demag* d, int* kmode) {
+    if (!d || !kmode) { set_error("null argument"); return MXB_EINVAL; }
+    *kmode = d->plan.kmode;
+    return MXB_OK;
+}
+
 int mxb_demag_set_fast(mxb_demag* d, int fast) {
     if (!d) { set_error("null argument"); return MXB_EINVAL; }
     if (d->plan.pipe && !fast) {

@@ -94,6 +94,13 @@ class DemagKernel:
         L.check(L.load().mxb_demag_get_spectra(self._d.h, L.dptr(out)), "get_spectra")
         return out[..., 0] + 1j * out[..., 1]
 
+    @property
+    def pipeline(self) -> bool:
+        """True when the y/z passes run as the L2-resident plane pipeline (yz_pipe.cu)."""
+        k = C.c_int()
+        L.check(L.load().mxb_demag_kmode(self._d.h, C.byref(k)), "kmode")
+        return k.value == 3
+
     def set_fast(self, flag: bool) -> None:
         """Use the register-resident radix-16 kernels (default) or the generic
         mixed-radix kernels where both cover the shape."""
