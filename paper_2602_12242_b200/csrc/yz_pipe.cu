@@ -1,31 +1,41 @@
 // L2-resident y/z pipeline over kx planes (single GPU, 3-D, symmetric kernel).
 //
 // The 5-pass demag evaluation moves every intermediate through HBM; at 512^3
-// the y/z middle (y forward, z fused, y inverse) alone is ~79 GB per
-// evaluation.  Here one persistent cooperative kernel walks the hx kx-planes
-// in ticks.  In tick t it runs, spread over all CTAs,
-//   A  y forward of plane t      : XP rows (HBM) -> slot[t % 3]   [z][ky][c]
-//   B  z fwd * K * z inv, plane t-1 : in place in slot[(t-1) % 3]
-//   C  y inverse of plane t-2    : slot[(t-2) % 3] -> XP rows (HBM)
-// and a grid barrier separates ticks.  The three slots (3 * nz * py * 48 B,
-// 75 MB at 512^3) stay in L2, so HBM only sees XP once each way plus the
-// kernel spectra: ~19 GB per evaluation at 512^3.
+// the y/z middle (y forward, z fused, y inverse) alone is ~72 GB per
+// evaluation although one kx plane of it (nz x py x 3 complex = 25 MB) fits in
+// L2.  Here one persistent cooperative kernel processes work units of the hx
+// kx-planes in dataflow order:
+//   A(p, z)   y forward of row z of plane p : XP (HBM) -> slot[p % 3] [z][ky][c]
+//   B(p, ky)  z forward * K * z inverse of column ky, in place in slot[p % 3]
+//   C(p, z)   y inverse of row z            : slot[p % 3] -> XP (HBM, in place)
+// with dependencies B(p, .) <- all A(p, .), C(p, .) <- all B(p, .) and
+// A(p, z) <- C(p-3, z) (the slot row is reused three planes later).  The
+// three slots (3 * nz * py * 48 B, 75 MB at 512^3) are meant to stay in L2, so
+// HBM sees XP once each way plus the kernel spectra.
+//
+// Scheduling: an atomic ticket counter hands units out in rounds
+//   round r = A(r) | B(r-1), first half of ky | C(r-2) | B(r-1), second half
+// so that in steady state every dependency lies about one thousand tickets
+// back (more than the units in flight): waits are rare.  Completion is
+// counted per plane (A, B) and per slot row (C: a generation counter), polled
+// with ld.acquire by one thread.  The per-unit round trips to L2 are kept off
+// the critical path: the ticket after next is fetched early, the next unit's
+// readiness is polled before the staging wait, and a unit's completion is
+// signalled only after the next unit's staging wait (its stores have drained
+// by then; immediately before any blocking wait, so signals cannot form a
+// cycle between CTAs).  A wait longer than 2 s raises an abort word that makes
+// every CTA leave: a scheduling bug cannot hang the device.
 //
 // Layouts: XP[kx][z][y][c] (plane-major x-pass output, written by
 // k_r2c_fast with CH = CHP = 1), Kp[kx][ky'][kz'][6] real quarter spectra
 // with ky' = min(ky, py-ky), kz' = min(kz, pz-kz) and the parity signs of
-// XY/XZ/YZ (as k_quarterize).  The transforms are the same register-resident
-// radix-16 Stockham code (fft_fast.cuh) with the same twiddles as the 5-pass
-// kernels, so both paths produce identical results.
-//
-// Every unit is one line triple (the 3 components): 3 * L/16 threads, two
-// CTAs per SM.  HBM-sourced inputs (XP rows for A, K rows for B) are
-// prefetched with cp.async into a staging buffer while the previous unit
-// computes; slot traffic (L2) is loaded and stored cooperatively through
-// shared memory so every warp access is contiguous.
+// XY/XZ/YZ (as k_quarterize).  k_yz_pipe uses the same register-resident
+// radix-16 Stockham code (fft_fast.cuh) and twiddles as the 5-pass kernels, so
+// both paths give identical results; k_yz_pipe_w (L = 1024, opt-in) uses the
+// warp-per-line core of fft_warp.cuh.
 #include <stdio.h>
-#include <type_traits>
 #include <stdlib.h>
+#include <type_traits>
 
 #include "demag.cuh"
 #include "fft_fast.cuh"
@@ -43,7 +53,7 @@ struct PipeArgs {
     double2* XP;          // [hx][nz][ny][3], input and output (in place)
     double2* slot;        // 3 x [nz][L][3]
     const double* Kp;     // [hx][L/2+1][L/2+1][6]
-    unsigned* sync;       // [ticket, abort, doneA[hx], doneB[hx], doneC[hx]], zeroed per launch
+    unsigned* sync;       // [ticket, abort, doneA[hx], doneB[hx], rowgen[3][n]], zeroed per launch
     int hx, n;            // planes; non-zero rows ny == nz == n
     double scale;
 };
@@ -74,60 +84,72 @@ struct Unit {
     int kind, plane, idx;
 };
 
-// Tickets are handed out in rounds r = 0 .. hx+1; round r holds, in order,
-//   A(r) [n units, r < hx], C(r-2) [n units, 2 <= r], B(r-1) [L units, 1 <= r <= hx].
-// Every dependency (B(p) <- A(p), C(p) <- B(p), A(p) <- C(p-3) for the slot
-// reuse) then lies in the previous round at least n tickets back, so with
-// n >= the number of CTAs a unit almost never waits.
 __device__ __forceinline__ int ky_of(int q, int L) {
     // pair ky with L - ky on neighbouring tickets: the shared K row is read once from HBM
     return q == 0 ? 0 : ((q & 1) ? (q + 1) / 2 : L - q / 2);
 }
 
-// ticket -> unit (hx >= 2): round 0 = A(0); round 1 = A(1), B(0);
-// rounds 2..hx-1 = A(r), C(r-2), B(r-1); round hx = C(hx-2), B(hx-1); round hx+1 = C(hx-1)
-__device__ __forceinline__ Unit decode(long long k, int hx, int n, int L) {
-    if (k < n) return {U_A, 0, (int)k};
-    k -= n;
-    if (k < n) return {U_A, 1, (int)k};
-    k -= n;
-    if (k < L) return {U_B, 0, ky_of((int)k, L)};
-    k -= L;
-    const long long full = 2LL * n + L, nfull = hx - 2;
-    if (k < nfull * full) {
-        const int r = 2 + (int)(k / full);
-        int o = (int)(k % full);
-        if (o < n) return {U_A, r, o};
-        o -= n;
-        if (o < n) return {U_C, r - 2, o};
-        return {U_B, r - 1, ky_of(o - n, L)};
+// ticket -> unit.  Round r (0 <= r <= hx+1) holds, in order:
+//   A(r) [n, r < hx], B(r-1) q < L/2 [1 <= r <= hx], C(r-2) [n, r >= 2], B(r-1) q >= L/2
+struct TicketMap {
+    int hx, n, L;
+    __device__ Unit operator()(long long k) const {
+        const int h = L / 2;
+        if (k < 0) return {U_NONE, 0, 0};
+        // rounds 0 and 1
+        if (k < n) return {U_A, 0, (int)k};
+        k -= n;
+        if (hx > 1) {
+            if (k < n) return {U_A, 1, (int)k};
+            k -= n;
+        }
+        if (k < L) return {U_B, 0, ky_of((int)k, L)};
+        k -= L;
+        // full rounds 2 .. hx-1
+        const long long full = 2LL * n + L, nfull = hx > 2 ? hx - 2 : 0;
+        if (k < nfull * full) {
+            const int r = 2 + (int)(k / full);
+            int o = (int)(k % full);
+            if (o < n) return {U_A, r, o};
+            o -= n;
+            if (o < h) return {U_B, r - 1, ky_of(o, L)};
+            o -= h;
+            if (o < n) return {U_C, r - 2, o};
+            return {U_B, r - 1, ky_of(h + o - n, L)};
+        }
+        k -= nfull * full;
+        // round hx: B(hx-1) first half, C(hx-2), B(hx-1) second half (hx >= 2)
+        if (hx >= 2) {
+            if (k < h) return {U_B, hx - 1, ky_of((int)k, L)};
+            k -= h;
+            if (k < n) return {U_C, hx - 2, (int)k};
+            k -= n;
+            if (k < h) return {U_B, hx - 1, ky_of(h + (int)k, L)};
+            k -= h;
+        }
+        // round hx+1: C(hx-1)
+        if (k < n) return {U_C, hx - 1, (int)k};
+        return {U_NONE, 0, 0};
     }
-    k -= nfull * full;
-    if (k < n) return {U_C, hx - 2, (int)k};
-    k -= n;
-    if (k < L) return {U_B, hx - 1, ky_of((int)k, L)};
-    k -= L;
-    if (k < n) return {U_C, hx - 1, (int)k};
-    return {U_NONE, 0, 0};
-}
+};
 
-// ticket / dependency bookkeeping shared by the pipeline kernels
+// dependency bookkeeping: doneA / doneB per plane, rowgen[slot][z] = number of
+// C units that have drained slot row z (A(p, z) needs rowgen[p % 3][z] >= p / 3)
 struct Sched {
-    unsigned *ticket, *abort_w, *doneA, *doneB, *doneC;
+    unsigned *ticket, *abort_w, *doneA, *doneB, *rowgen;
     int n, L;
     __device__ Sched(const PipeArgs& a, int L_) : n(a.n), L(L_) {
         ticket = a.sync;
         abort_w = a.sync + 1;
         doneA = a.sync + 2;
         doneB = doneA + a.hx;
-        doneC = doneB + a.hx;
+        rowgen = doneB + a.hx;
     }
-    // counter a unit waits on, and its target
     __device__ bool dep(const Unit& u, const unsigned** c, unsigned* target) const {
         if (u.kind == U_A) {
             if (u.plane < 3) return false;
-            *c = doneC + (u.plane - 3);
-            *target = (unsigned)n;
+            *c = rowgen + (u.plane % 3) * n + u.idx;
+            *target = (unsigned)(u.plane / 3);
         } else if (u.kind == U_B) {
             *c = doneA + u.plane;
             *target = (unsigned)n;
@@ -137,26 +159,44 @@ struct Sched {
         }
         return true;
     }
-    __device__ bool ready(const Unit& u) const {   // thread 0
+    __device__ const unsigned* done_of(const Unit& u) const {
+        if (u.kind == U_A) return doneA + u.plane;
+        if (u.kind == U_B) return doneB + u.plane;
+        return rowgen + (u.plane % 3) * n + u.idx;
+    }
+    // thread 0: non-blocking readiness
+    __device__ bool ready(const Unit& u) const {
         const unsigned* c;
         unsigned tg;
-        return !dep(u, &c, &tg) || ld_acquire(c) >= tg;
+        return u.kind != U_NONE && (!dep(u, &c, &tg) || ld_acquire(c) >= tg);
     }
-    // thread 0 waits (2 s cap, then every CTA leaves: results are then garbage
-    // but the device stays usable); CTA-wide, returns false on abort
-    __device__ bool wait_ready(const Unit& u, int* flag) const {
+    // after a __syncthreads that follows the unit's stores; thread 0
+    __device__ void signal(const Unit& u) const {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(const_cast<unsigned*>(done_of(u)), 1u);
+        }
+    }
+    // CTA-wide wait for u's inputs.  Never blocks while holding an unsignalled
+    // unit (deferred signals could otherwise form a cycle between CTAs);
+    // pending is thread 0's.  Returns false on abort.
+    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending) const {
         if (threadIdx.x == 0) {
             *flag = 1;
             const unsigned* c;
             unsigned tg;
-            if (dep(u, &c, &tg)) {
+            if (dep(u, &c, &tg) && ld_acquire(c) < tg) {
+                if (pending.kind != U_NONE) {
+                    signal(pending);
+                    pending.kind = U_NONE;
+                }
                 const unsigned long long t0 = gtimer();
                 while (ld_acquire(c) < tg) {
                     __nanosleep(32);
                     if (ld_acquire(abort_w)) { *flag = 0; break; }
                     if (gtimer() - t0 > 2000000000ull) {
-                        printf("k_yz_pipe: wait timeout cta %d kind %d plane %d have %u need %u\n", blockIdx.x,
-                               u.kind, u.plane, ld_acquire(c), tg);
+                        printf("k_yz_pipe: wait timeout cta %d kind %d plane %d idx %d have %u need %u\n",
+                               blockIdx.x, u.kind, u.plane, u.idx, ld_acquire(c), tg);
                         atomicExch(abort_w, 1u);
                         *flag = 0;
                         break;
@@ -166,23 +206,6 @@ struct Sched {
         }
         __syncthreads();
         return *flag != 0;
-    }
-    __device__ const unsigned* done_of(const Unit& u) const {
-        return (u.kind == U_A ? doneA : (u.kind == U_B ? doneB : doneC)) + u.plane;
-    }
-    // does u wait on the counter p signals?
-    __device__ bool waits_on(const Unit& u, const Unit& p) const {
-        const unsigned* c;
-        unsigned tg;
-        return p.kind != U_NONE && dep(u, &c, &tg) && c == done_of(p);
-    }
-    // after a __syncthreads that follows the unit's stores
-    __device__ void signal(const Unit& u) const {
-        if (threadIdx.x == 0) {
-            __threadfence();
-            unsigned* c = u.kind == U_A ? doneA : (u.kind == U_B ? doneB : doneC);
-            atomicAdd(c + u.plane, 1u);
-        }
     }
 };
 
@@ -201,7 +224,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     constexpr int R = PipeCfg<L>::R, TPL = PipeCfg<L>::TPL, T = PipeCfg<L>::T;
     constexpr int L2 = L / 2 + 1;
     extern __shared__ double2 sm[];
-    __shared__ long long next_ticket;
+    __shared__ long long tk_sh;   // ticket of the unit after next
     __shared__ int flag;
     double2* X = sm;
     double2* S = sm + PipeCfg<L>::XE;
@@ -210,6 +233,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     const long long slot_e = (long long)n * L * 3;         // slot elements
     const int b = threadIdx.x / TPL, t = threadIdx.x - (threadIdx.x / TPL) * TPL;
     const Sched sc(a, L);
+    const TicketMap tmap{hx, n, L};
 
     // unit inputs, staged in S with cp.async: A an XP row (HBM), B a slot
     // column (L2), C a slot row (L2); B also stages its K rows (HBM) over its
@@ -237,25 +261,44 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
         cp_async_commit();
     };
 
-    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
+    // thread 0's private state: the unsignalled previous unit and the ticket
+    // being fetched for the unit after next
+    Unit pending{U_NONE, 0, 0};
+    long long tk2 = -1;
+    if (threadIdx.x == 0) {
+        const long long t0 = atomicAdd(sc.ticket, 1u);
+        tk_sh = atomicAdd(sc.ticket, 1u);
+        flag = (int)t0;
+    }
     __syncthreads();
-    Unit cur = decode(next_ticket, hx, n, L);
+    Unit cur = tmap(flag);
+    Unit nxt = tmap(tk_sh);
     bool staged = false;
 
     while (cur.kind != U_NONE) {
         if (!staged) {
-            if (!sc.wait_ready(cur, &flag)) return;
+            if (!sc.wait_ready(cur, &flag, pending)) return;
             stage_in(cur);
         }
-        __syncthreads();   // next_ticket / flag are free
-        if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
+        // round trips issued now, consumed later: the ticket after next, and
+        // (below) nxt's readiness
+        bool nxt_ready = false;
+        if (threadIdx.x == 0) {
+            tk2 = atomicAdd(sc.ticket, 1u);
+            nxt_ready = sc.ready(nxt);
+        }
         double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
         const int nin = cur.kind == U_C ? L : n;
         double2 v[R];
         cp_async_wait_all();
+        if (threadIdx.x == 0) {
+            if (pending.kind != U_NONE) {
+                sc.signal(pending);
+                pending.kind = U_NONE;
+            }
+            flag = nxt_ready;
+        }
         __syncthreads();
-        const Unit nxt = decode(next_ticket, hx, n, L);
-        if (threadIdx.x == 0) flag = nxt.kind != U_NONE && sc.ready(nxt);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int e = t + m * TPL;
@@ -337,121 +380,17 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
             double2* dst = a.XP + cur.plane * plane_xp + (long long)cur.idx * n * 3;
             for (int j = threadIdx.x; j < 3 * n; j += T) st_stream(dst + j, X[j]);
         }
+        if (threadIdx.x == 0) {
+            tk_sh = tk2;
+            pending = cur;
+        }
         __syncthreads();
-        sc.signal(cur);
         cur = nxt;
+        nxt = tmap(tk_sh);
         staged = staged_next;
     }
+    if (threadIdx.x == 0 && pending.kind != U_NONE) sc.signal(pending);
 }
-
-
-
-// ---------------------------------------------------------------------------
-// warp kernel scheduling.  Round r = A(r) [n], B(r-1) [L], C(r-2) [n].  A slot
-// row is rewritten by A(r, z) only after C(r-3, z) has read it: a per-row
-// generation counter rowgen[r % 3][z] (C increments it), so every dependency
-// lies at least n tickets back (B and C: about a full round).
-// sync words: [ticket, abort, doneA[hx], doneB[hx], rowgen[3][n]]
-// ---------------------------------------------------------------------------
-// rounds 0 and 1 and the two tail rounds are partial; tickets skip the empty
-// parts so that the numbering stays dense
-struct TicketMap {
-    int hx, n, L;
-    __device__ Unit operator()(long long k) const {
-        // round 0: A(0)
-        if (k < n) return {U_A, 0, (int)k};
-        k -= n;
-        // round 1: A(1), B(0)
-        if (k < n) return {U_A, 1, (int)k};
-        k -= n;
-        if (k < L) return {U_B, 0, ky_of((int)k, L)};
-        k -= L;
-        // full rounds 2 .. hx-1: A(r), B(r-1), C(r-2)
-        const long long full = 2LL * n + L, nfull = hx - 2;
-        if (k < nfull * full) {
-            const int r = 2 + (int)(k / full);
-            int o = (int)(k % full);
-            if (o < n) return {U_A, r, o};
-            o -= n;
-            if (o < L) return {U_B, r - 1, ky_of(o, L)};
-            return {U_C, r - 2, o - L};
-        }
-        k -= nfull * full;
-        // round hx: B(hx-1), C(hx-2); round hx+1: C(hx-1)
-        if (k < L) return {U_B, hx - 1, ky_of((int)k, L)};
-        k -= L;
-        if (k < n) return {U_C, hx - 2, (int)k};
-        k -= n;
-        if (k < n) return {U_C, hx - 1, (int)k};
-        return {U_NONE, 0, 0};
-    }
-};
-
-struct SchedW {
-    unsigned *ticket, *abort_w, *doneA, *doneB, *rowgen;
-    int n, L;
-    __device__ SchedW(const PipeArgs& a, int L_) : n(a.n), L(L_) {
-        ticket = a.sync;
-        abort_w = a.sync + 1;
-        doneA = a.sync + 2;
-        doneB = doneA + a.hx;
-        rowgen = doneB + a.hx;
-    }
-    __device__ bool dep(const Unit& u, const unsigned** c, unsigned* target) const {
-        if (u.kind == U_A) {
-            if (u.plane < 3) return false;
-            *c = rowgen + (u.plane % 3) * n + u.idx;
-            *target = (unsigned)(u.plane / 3);
-        } else if (u.kind == U_B) {
-            *c = doneA + u.plane;
-            *target = (unsigned)n;
-        } else {
-            *c = doneB + u.plane;
-            *target = (unsigned)L;
-        }
-        return true;
-    }
-    __device__ const unsigned* done_of(const Unit& u) const {
-        if (u.kind == U_A) return doneA + u.plane;
-        if (u.kind == U_B) return doneB + u.plane;
-        return rowgen + (u.plane % 3) * n + u.idx;
-    }
-    // never block while holding an unsignalled unit: deferred signals could
-    // otherwise form a cycle between CTAs.  pending is thread 0's.
-    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending) const {
-        if (threadIdx.x == 0) {
-            *flag = 1;
-            const unsigned* c;
-            unsigned tg;
-            if (dep(u, &c, &tg) && ld_acquire(c) < tg) {
-                if (pending.kind != U_NONE) {
-                    signal(pending);
-                    pending.kind = U_NONE;
-                }
-                const unsigned long long t0 = gtimer();
-                while (ld_acquire(c) < tg) {
-                    __nanosleep(32);
-                    if (ld_acquire(abort_w)) { *flag = 0; break; }
-                    if (gtimer() - t0 > 2000000000ull) {
-                        printf("k_yz_pipe_w: wait timeout cta %d kind %d plane %d idx %d have %u need %u\n",
-                               blockIdx.x, u.kind, u.plane, u.idx, ld_acquire(c), tg);
-                        atomicExch(abort_w, 1u);
-                        *flag = 0;
-                        break;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        return *flag != 0;
-    }
-    __device__ void signal(const Unit& u) const {
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(const_cast<unsigned*>(done_of(u)), 1u);
-        }
-    }
-};
 
 // ---------------------------------------------------------------------------
 // warp-FFT variant, L = 1024 (n = 512): one line per warp (fft_warp.cuh), the
@@ -473,7 +412,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * L;
-    const SchedW sc(a, L);
+    const Sched sc(a, L);
     const TicketMap tmap{hx, N, L};
 
     auto stage = [&](const Unit& u) {
@@ -629,7 +568,7 @@ static int pipe_launch_L(const PipeArgs& a, const double2* tw, cudaStream_t st, 
     }
     int g = grid;
     if (const char* e = getenv("MXB_PIPE_GRID")) g = atoi(e) > 0 ? atoi(e) : g;
-    MXB_CUDA(cudaMemsetAsync(a.sync, 0, (2 + 3 * (size_t)a.hx) * sizeof(unsigned), st));
+    MXB_CUDA(cudaMemsetAsync(a.sync, 0, (2 + 2 * (size_t)a.hx + 3 * (size_t)a.n) * sizeof(unsigned), st));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3((unsigned)T);
