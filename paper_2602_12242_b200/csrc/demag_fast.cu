@@ -258,7 +258,7 @@ k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict_
 // ---------------------------------------------------------------------------
 // x rows: r2c of real length 2M through a complex FFT of length M
 // ---------------------------------------------------------------------------
-template <int M>
+template <int M, bool PM>
 __global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
 k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in2,
            double2* __restrict__ out, int CH, int CHP, long long BLKE, long long nrows,
@@ -303,8 +303,20 @@ k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in
         for (int i = 0; i < R; ++i) X[sidx<false, M, R, NL>(b, out_elem<M, R>(t, i))] = v[i];
         __syncthreads();
         for (int u = threadIdx.x; u < NR * HX * 3; u += T) {
-            const int url = u / (HX * 3), qq = u - url * (HX * 3);
-            const int kx = qq / 3, cc = qq - 3 * kx;
+            // row-major output: walk (row, kx, c) so a warp writes along kx; plane-major
+            // (CH = 1): walk (kx, row, c) so each plane gets NR*48 contiguous bytes
+            int url, kx, cc;
+            if (PM) {   // CH == 1
+                kx = u / (NR * 3);
+                const int r = u - kx * (NR * 3);
+                url = r / 3;
+                cc = r - 3 * url;
+            } else {
+                url = u / (HX * 3);
+                const int qq = u - url * (HX * 3);
+                kx = qq / 3;
+                cc = qq - 3 * kx;
+            }
             const long long urow = tile * NR + url;
             if (urow >= nrows) continue;
             const int ub = 3 * url + cc;
@@ -319,7 +331,7 @@ k_r2c_fast(const double* __restrict__ in, long long cstride, int pitch, int n_in
     }
 }
 
-template <int M>
+template <int M, bool PM>
 __global__ void __launch_bounds__(3 * Cfg<M>::NRr * Cfg<M>::TPL, 2)
 k_c2r_fast(const double2* __restrict__ Xin, int CH, int CHP, long long BLKE, double* __restrict__ out,
            long long cstride, int pitch, int n_out2, long long nrows, const double2* __restrict__ twM,
@@ -334,12 +346,25 @@ k_c2r_fast(const double2* __restrict__ Xin, int CH, int CHP, long long BLKE, dou
     const int T = blockDim.x;
     auto prefetch = [&](long long tile) {
         for (int u = threadIdx.x; u < NR * HX * 3; u += T) {
-            const int url = u / (HX * 3), qq = u - url * (HX * 3);
+            // staged as S[url][kx][c]; plane-major input (CH = 1) is read kx-major so
+            // consecutive threads fetch contiguous bytes of one plane
+            int url, kx, cc;
+            if (PM) {   // CH == 1
+                kx = u / (NR * 3);
+                const int r = u - kx * (NR * 3);
+                url = r / 3;
+                cc = r - 3 * url;
+            } else {
+                url = u / (HX * 3);
+                const int qq = u - url * (HX * 3);
+                kx = qq / 3;
+                cc = qq - 3 * kx;
+            }
             const long long row = tile * NR + url;
             const bool ok = row < nrows;
-            const int kx = qq / 3, blk = kx / CH;
-            const long long src = blk * BLKE + ((ok ? row : 0) * CHP + (kx - blk * CH)) * 3 + (qq - 3 * kx);
-            cp_async16(&S[u], Xin + src, ok);
+            const int blk = kx / CH;
+            const long long src = blk * BLKE + ((ok ? row : 0) * CHP + (kx - blk * CH)) * 3 + cc;
+            cp_async16(&S[(url * HX + kx) * 3 + cc], Xin + src, ok);
         }
         cp_async_commit();
     };
@@ -504,14 +529,23 @@ static int rows_launch(bool fwd, const double* in_r, double2* X, double* out_r, 
     const long long ntiles = (nrows + NR - 1) / NR;
     const int thr = NL * Cfg<M>::TPL;
     int grid = 0, rc;
-    if (fwd) {
-        if ((rc = persistent_grid(k_r2c_fast<M>, thr, sm, ntiles, &grid))) return rc;
-        k_r2c_fast<M><<<grid, thr, sm, st>>>(in_r, cstride, pitch, nhalf, X, CH, CHP, BLKE, nrows, twM,
-                                             tw2M, halt);
+    // plane-major layout (one kx per block, CH = 1): walk kx-major
+    if (fwd && CH == 1) {
+        if ((rc = persistent_grid(k_r2c_fast<M, true>, thr, sm, ntiles, &grid))) return rc;
+        k_r2c_fast<M, true><<<grid, thr, sm, st>>>(in_r, cstride, pitch, nhalf, X, CH, CHP, BLKE, nrows, twM,
+                                                   tw2M, halt);
+    } else if (fwd) {
+        if ((rc = persistent_grid(k_r2c_fast<M, false>, thr, sm, ntiles, &grid))) return rc;
+        k_r2c_fast<M, false><<<grid, thr, sm, st>>>(in_r, cstride, pitch, nhalf, X, CH, CHP, BLKE, nrows, twM,
+                                                    tw2M, halt);
+    } else if (CH == 1) {
+        if ((rc = persistent_grid(k_c2r_fast<M, true>, thr, sm, ntiles, &grid))) return rc;
+        k_c2r_fast<M, true><<<grid, thr, sm, st>>>(X, CH, CHP, BLKE, out_r, cstride, pitch, nhalf, nrows, twM,
+                                                   tw2M, halt);
     } else {
-        if ((rc = persistent_grid(k_c2r_fast<M>, thr, sm, ntiles, &grid))) return rc;
-        k_c2r_fast<M><<<grid, thr, sm, st>>>(X, CH, CHP, BLKE, out_r, cstride, pitch, nhalf, nrows, twM,
-                                             tw2M, halt);
+        if ((rc = persistent_grid(k_c2r_fast<M, false>, thr, sm, ntiles, &grid))) return rc;
+        k_c2r_fast<M, false><<<grid, thr, sm, st>>>(X, CH, CHP, BLKE, out_r, cstride, pitch, nhalf, nrows, twM,
+                                                    tw2M, halt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
