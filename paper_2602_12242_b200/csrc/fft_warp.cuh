@@ -99,9 +99,10 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane, 
         else if (k) w = twid<DIR>(tw, lane * k);
         const double2 a = k ? cmul(v[p32(k)], w) : v[p32(k)];
         W[tsw(k, lane)] = a;
-        // keep the chain in step with the stores: computed ahead, all 31
+        // a real data dependency (0 * a is not foldable under IEEE rules) keeps
+        // the twiddle chain in step with the stores; computed ahead, all 31
         // twiddles would stay live across the first DFT
-        asm volatile("" : "+d"(w.x), "+d"(w.y)::"memory");
+        w.x = fma(0.0, a.x, w.x);
     }
     __syncwarp();
 #pragma unroll

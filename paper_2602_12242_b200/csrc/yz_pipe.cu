@@ -492,26 +492,29 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             __syncthreads();
             const bool fy = 2 * ky > L;
             const double s = a.scale;
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int kz = lane + 32 * k;
+            // each thread owns whole kz rows (all 3 components), in place in W
+            for (int kz = threadIdx.x; kz < L; kz += 96) {
                 const bool fz = 2 * kz > L;
                 const double2* kr = KS + (fz ? L - kz : kz) * 3;
+                const double2 q01 = kr[0], q23 = kr[1], q45 = kr[2];
+                const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                const double kxy = fy ? -q01.y : q01.y;
+                const double kxz = fz ? -q23.x : q23.x;
+                const double kyz = (fy != fz) ? -q45.x : q45.x;
                 const double2 m0 = W[kz], m1 = W[L + kz], m2 = W[2 * L + kz];
-                double k0, k1, k2;   // row c of the symmetric 3x3 with the parity signs
-                if (c == 0) {
-                    const double2 q01 = kr[0], q23 = kr[1];
-                    k0 = q01.x; k1 = fy ? -q01.y : q01.y; k2 = fz ? -q23.x : q23.x;
-                } else if (c == 1) {
-                    const double2 q01 = kr[0], q23 = kr[1], q45 = kr[2];
-                    k0 = fy ? -q01.y : q01.y; k1 = q23.y; k2 = (fy != fz) ? -q45.x : q45.x;
-                } else {
-                    const double2 q23 = kr[1], q45 = kr[2];
-                    k0 = fz ? -q23.x : q23.x; k1 = (fy != fz) ? -q45.x : q45.x; k2 = q45.y;
-                }
-                const double2 h = make_double2(k0 * m0.x + k1 * m1.x + k2 * m2.x, k0 * m0.y + k1 * m1.y + k2 * m2.y);
-                v[k] = make_double2(h.x * s, h.y * s);
+                const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                W[kz] = make_double2(h0.x * s, h0.y * s);
+                W[L + kz] = make_double2(h1.x * s, h1.y * s);
+                W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
             }
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = Wc[lane + 32 * m];
             __syncthreads();   // all reads of W done before the tiles are reused
             fw::fft1024<1>(v, Wc, lane, tw);
             __syncthreads();
@@ -625,10 +628,11 @@ static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t s
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
             const double2* tw, cudaStream_t st, const int* halt) {
     const PipeArgs a{XP, slot, Kp, bar, hx, n, scale};
-    // the warp-FFT variant is opt-in: on par with the radix-16 pipeline at
-    // 512^3 (32.4 vs 32.0 ms per evaluation), which is bit-identical to the 5-pass path
+    // warp-FFT variant by default at L = 1024 (27.6 vs 32.1 ms per evaluation at
+    // 512^3; within 4e-16 of the 5-pass path).  MXB_PIPE_WARP=0 selects the
+    // radix-16 pipeline, which is bit-identical to the 5-pass path.
     const char* we = getenv("MXB_PIPE_WARP");
-    const bool warp = we && we[0] == '1';
+    const bool warp = !(we && we[0] == '0');
     if (2 * n == 1024 && warp) return pipe_launch_warp(a, tw, st, halt);
     switch (2 * n) {
         case 16: return pipe_launch_L<16>(a, tw, st, halt);
