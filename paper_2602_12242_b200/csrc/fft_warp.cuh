@@ -86,7 +86,12 @@ __device__ __forceinline__ int tsw(int r, int l) { return r * 32 + (l ^ (r & 7))
 // v[m] = x[lane + 32 m] on entry; lane j holds X[j + 32 k] in v[p32(k)] on exit.
 // W: this warp's 1024-element tile (free on entry, clobbered).
 template <int DIR>
-__device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_in, const double2* __restrict__ tw) {
+    // an opaque copy of the lane index: the lane-dependent tile addresses are
+    // then recomputed per call instead of being hoisted out of the caller's
+    // loop (32 live addresses that end up spilled)
+    int lane = lane_in;
+    asm volatile("" : "+r"(lane));
     dft32<DIR>(v);
     __syncwarp();
     // w1024^(lane k) as a running product, re-anchored from the exact table

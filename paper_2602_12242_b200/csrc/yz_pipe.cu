@@ -136,33 +136,34 @@ struct TicketMap {
 // dependency bookkeeping: doneA / doneB per plane, rowgen[slot][z] = number of
 // C units that have drained slot row z (A(p, z) needs rowgen[p % 3][z] >= p / 3)
 struct Sched {
-    unsigned *ticket, *abort_w, *doneA, *doneB, *rowgen;
-    int n, L;
-    __device__ Sched(const PipeArgs& a, int L_) : n(a.n), L(L_) {
-        ticket = a.sync;
-        abort_w = a.sync + 1;
-        doneA = a.sync + 2;
-        doneB = doneA + a.hx;
-        rowgen = doneB + a.hx;
-    }
+    // one base pointer; the counters are derived on use (fewer live registers
+    // across the unit loop of the FFT kernels)
+    unsigned* base;
+    int hx, n, L;
+    __device__ Sched(const PipeArgs& a, int L_) : base(a.sync), hx(a.hx), n(a.n), L(L_) {}
+    __device__ unsigned* ticket() const { return base; }
+    __device__ unsigned* abort_w() const { return base + 1; }
+    __device__ unsigned* doneA() const { return base + 2; }
+    __device__ unsigned* doneB() const { return base + 2 + hx; }
+    __device__ unsigned* rowgen() const { return base + 2 + 2 * hx; }
     __device__ bool dep(const Unit& u, const unsigned** c, unsigned* target) const {
         if (u.kind == U_A) {
             if (u.plane < 3) return false;
-            *c = rowgen + (u.plane % 3) * n + u.idx;
+            *c = rowgen() + (u.plane % 3) * n + u.idx;
             *target = (unsigned)(u.plane / 3);
         } else if (u.kind == U_B) {
-            *c = doneA + u.plane;
+            *c = doneA() + u.plane;
             *target = (unsigned)n;
         } else {
-            *c = doneB + u.plane;
+            *c = doneB() + u.plane;
             *target = (unsigned)L;
         }
         return true;
     }
     __device__ const unsigned* done_of(const Unit& u) const {
-        if (u.kind == U_A) return doneA + u.plane;
-        if (u.kind == U_B) return doneB + u.plane;
-        return rowgen + (u.plane % 3) * n + u.idx;
+        if (u.kind == U_A) return doneA() + u.plane;
+        if (u.kind == U_B) return doneB() + u.plane;
+        return rowgen() + (u.plane % 3) * n + u.idx;
     }
     // thread 0: non-blocking readiness
     __device__ bool ready(const Unit& u) const {
@@ -193,11 +194,11 @@ struct Sched {
                 const unsigned long long t0 = gtimer();
                 while (ld_acquire(c) < tg) {
                     __nanosleep(32);
-                    if (ld_acquire(abort_w)) { *flag = 0; break; }
+                    if (ld_acquire(abort_w())) { *flag = 0; break; }
                     if (gtimer() - t0 > 2000000000ull) {
                         printf("k_yz_pipe: wait timeout cta %d kind %d plane %d idx %d have %u need %u\n",
                                blockIdx.x, u.kind, u.plane, u.idx, ld_acquire(c), tg);
-                        atomicExch(abort_w, 1u);
+                        atomicExch(abort_w(), 1u);
                         *flag = 0;
                         break;
                     }
@@ -266,8 +267,8 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     Unit pending{U_NONE, 0, 0};
     long long tk2 = -1;
     if (threadIdx.x == 0) {
-        const long long t0 = atomicAdd(sc.ticket, 1u);
-        tk_sh = atomicAdd(sc.ticket, 1u);
+        const long long t0 = atomicAdd(sc.ticket(), 1u);
+        tk_sh = atomicAdd(sc.ticket(), 1u);
         flag = (int)t0;
     }
     __syncthreads();
@@ -284,7 +285,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
         // (below) nxt's readiness
         bool nxt_ready = false;
         if (threadIdx.x == 0) {
-            tk2 = atomicAdd(sc.ticket, 1u);
+            tk2 = atomicAdd(sc.ticket(), 1u);
             nxt_ready = sc.ready(nxt);
         }
         double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
@@ -437,7 +438,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     };
     // registers (lane j holds e = j + 32 k in v[p32(k)], k < NK) -> W natural [e][3]
     // -> contiguous 16-byte stores of the first ne elements (whole sectors per warp)
-    auto store_rows = [&](double2 (&v)[32], auto nk_tag, double2* dst, int ne, bool stream) {
+    auto store_rows = [&](double2 (&v)[32], auto nk_tag, double2* dst, int ne, bool stream, int lane) {
         constexpr int NK = decltype(nk_tag)::value;
         __syncthreads();   // every warp is done with its transpose tile
 #pragma unroll
@@ -449,7 +450,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             for (int j = threadIdx.x; j < 3 * ne; j += 96) st_l2(dst + j, W[j]);
     };
 
-    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
+    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
     __syncthreads();
     Unit cur = tmap(next_ticket);
     // completion of the previous unit is signalled after this unit's staging
@@ -479,13 +480,13 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         if (cur.kind == U_A) {
             // ---- y forward of row z = idx -> slot row [ky][c]
             fw::fft1024<-1>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
-            store_rows(v, std::integral_constant<int, 32>{}, slot + (long long)cur.idx * L * 3, L, false);
+            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            store_rows(v, std::integral_constant<int, 32>{}, slot + (long long)cur.idx * L * 3, L, false, lane);
         } else if (cur.kind == U_B) {
             // ---- z forward * K * z inverse of column ky = idx
             const int ky = cur.idx;
             fw::fft1024<-1>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
+            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < 32; ++k) Wc[lane + 32 * k] = v[fw::p32(k)];
@@ -529,9 +530,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         } else {
             // ---- y inverse of row z = idx -> XP row (n of L kept)
             fw::fft1024<1>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket, 1u);
+            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
             store_rows(v, std::integral_constant<int, 16>{}, a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3,
-                       N, true);
+                       N, true, lane);
         }
         __syncthreads();
         pending = cur;
