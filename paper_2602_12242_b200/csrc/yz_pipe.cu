@@ -44,6 +44,9 @@
 #ifndef MXB_PIPE_W_CTAS
 #define MXB_PIPE_W_CTAS 3
 #endif
+#ifndef MXB_PIPE_W_DIRECT_STORE
+#define MXB_PIPE_W_DIRECT_STORE 0
+#endif
 
 namespace mxb {
 
@@ -481,7 +484,15 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             // ---- y forward of row z = idx -> slot row [ky][c]
             fw::fft1024<-1>(v, Wc, lane, tw);
             if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+#if MXB_PIPE_W_DIRECT_STORE
+            {
+                double2* dst = slot + (long long)cur.idx * L * 3 + c;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) st_l2(dst + (long long)(lane + 32 * k) * 3, v[fw::p32(k)]);
+            }
+#else
             store_rows(v, std::integral_constant<int, 32>{}, slot + (long long)cur.idx * L * 3, L, false, lane);
+#endif
         } else if (cur.kind == U_B) {
             // ---- z forward * K * z inverse of column ky = idx
             const int ky = cur.idx;
@@ -531,8 +542,16 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             // ---- y inverse of row z = idx -> XP row (n of L kept)
             fw::fft1024<1>(v, Wc, lane, tw);
             if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+#if MXB_PIPE_W_DIRECT_STORE
+            {
+                double2* dst = a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3 + c;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) st_stream(dst + (long long)(lane + 32 * k) * 3, v[fw::p32(k)]);
+            }
+#else
             store_rows(v, std::integral_constant<int, 16>{}, a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3,
                        N, true, lane);
+#endif
         }
         __syncthreads();
         pending = cur;
