@@ -44,6 +44,9 @@
 #ifndef MXB_PIPE_W_CTAS
 #define MXB_PIPE_W_CTAS 3
 #endif
+#ifndef MXB_PIPE_DISCARD
+#define MXB_PIPE_DISCARD 1
+#endif
 #ifndef MXB_PIPE_W_DIRECT_STORE
 #define MXB_PIPE_W_DIRECT_STORE 0
 #endif
@@ -470,6 +473,15 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         }
         __syncthreads();
         double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
+#if MXB_PIPE_DISCARD
+        if (cur.kind == U_C) {
+            // the slot row is dead until A(p+3, z) rewrites it: drop its L2 lines
+            // without writing them back (48 KB = 384 lines of 128 B)
+            char* row = reinterpret_cast<char*>(slot + (long long)cur.idx * L * 3);
+            for (int j = threadIdx.x; j < 3 * L * 16 / 128; j += 96)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + (size_t)j * 128) : "memory");
+        }
+#endif
         double2 v[32];
         if (cur.kind == U_C) {
 #pragma unroll
