@@ -28,6 +28,11 @@ int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
               int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
               const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt);
 
+// warp-FFT x passes for nx = 512 (x_warp.cu); -1 when the shape is not covered
+int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, long long cstride, int pitch,
+              int nhalf, int CH, int CHP, long long BLKE, long long nrows, const double2* twM,
+              const double2* tw2M, cudaStream_t st, const int* halt);
+
 // L2-resident y/z pipeline over kx planes (yz_pipe.cu)
 bool pipe_shape_ok(int ny, int nz);
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,

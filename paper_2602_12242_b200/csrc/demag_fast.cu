@@ -608,6 +608,8 @@ int fast_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
               int pitch, int nhalf, int CH, int CHP, long long BLKE, long long nrows,
               const double2* twM, const double2* tw2M, cudaStream_t st, const int* halt) {
     if (!pow2(M)) return -1;
+    const int rw = warp_rows(fwd, M, in_r, X, out_r, cstride, pitch, nhalf, CH, CHP, BLKE, nrows, twM, tw2M, st, halt);
+    if (rw != -1) return rw;
 #define CASE(V) case V: return rows_launch<V>(fwd, in_r, X, out_r, cstride, pitch, nhalf, CH, CHP, BLKE, nrows, twM, tw2M, st, halt);
     switch (M) { MXB_POW2_CASES(CASE) default: return -1; }
 #undef CASE

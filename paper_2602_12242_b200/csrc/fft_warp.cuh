@@ -13,6 +13,7 @@
 // constant zero / never stored).
 #pragma once
 
+#include "fft_fast.cuh"
 #include "fft_generic.cuh"
 
 namespace mxb {
@@ -108,6 +109,38 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_i
         // the twiddle chain in step with the stores; computed ahead, all 31
         // twiddles would stay live across the first DFT
         w.x = fma(0.0, a.x, w.x);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < 32; ++l) v[l] = W[tsw(lane, l)];
+    dft32<DIR>(v);
+}
+
+
+// Two lines of length 512 = 32 x 16 per warp (the x passes: one line per row
+// and component).  Lane l holds xa[l + 32 m] in a[m] and xb[l + 32 m] in b[m]
+// (m < 16).  DFT-16 over m in registers, w512^(l k1) twiddles, one transpose
+// whose 32 tile rows are (line, k1), DFT-32 over l.  On exit lane j holds
+// X_line[k1 + 16 k2] in v[p32(k2)] with line = j >> 4, k1 = j & 15.
+template <int DIR>
+__device__ __forceinline__ void fft512x2(double2 (&a)[16], double2 (&b)[16], double2 (&v)[32], double2* W,
+                                         int lane_in, const double2* __restrict__ tw512) {
+    int lane = lane_in;
+    asm volatile("" : "+r"(lane));
+    ff::DFT<16, DIR>::run(a);
+    ff::DFT<16, DIR>::run(b);
+    __syncwarp();
+    const double2 w1 = twid<DIR>(tw512, lane);
+    double2 w = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k & 7) w = k == 1 ? w1 : cmul(w, w1);
+        else if (k) w = twid<DIR>(tw512, lane * k);
+        const double2 x = k ? cmul(a[k], w) : a[k];
+        const double2 y = k ? cmul(b[k], w) : b[k];
+        W[tsw(k, lane)] = x;
+        W[tsw(16 + k, lane)] = y;
+        w.x = fma(0.0, y.x, w.x);
     }
     __syncwarp();
 #pragma unroll

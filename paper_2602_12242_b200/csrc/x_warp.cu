@@ -1,0 +1,167 @@
+// x passes (P1 r2c / P5 c2r) with the warp-per-line FFT core, for rows of
+// nx = 512 reals (px = 1024, one complex FFT of M = 512 per row via the
+// half-length packing, as k_r2c_fast / k_c2r_fast in demag_fast.cu).
+//
+// A CTA is 3 warps, one per component; each warp transforms two rows of its
+// component (fw::fft512x2: register DFT-16s, one swizzled transpose,
+// register DFT-32s), so a CTA handles a row pair.  The r2c loads its packed
+// rows straight into registers (contiguous 16-byte pairs, whole sectors per
+// warp) and untangles the half-length spectrum through the warp's tile; the
+// outputs go out in 128-bin chunks staged in shared memory so every store
+// run is contiguous in either layout.  The c2r stages the spectrum rows of
+// its pair with cp.async, forms the packed input, and writes the real rows
+// straight from registers.  Layouts: row-major X[row][CHP][3] of one rank
+// (CH >= hx) or plane-major X[kx][row][3] (CH = 1, the plane pipeline).
+#include <stdlib.h>
+
+#include "demag.cuh"
+#include "fft_warp.cuh"
+
+namespace mxb {
+
+using namespace ff;
+
+namespace {
+constexpr int XM = 512;          // complex FFT length (px / 2)
+constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
+constexpr int XCHUNK = 128;      // r2c output staging chunk (bins)
+}
+
+template <bool PM>
+__global__ void __launch_bounds__(96, 3)
+k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __restrict__ out, int CHP,
+        long long BLKE, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
+        const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 W[];                 // 3 x 1024 transpose tiles
+    __shared__ double2 O[2 * XCHUNK * 3];          // [line][bin][c] output chunk
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* Wc = W + c * 1024;
+    const long long row0 = 2LL * blockIdx.x;
+    const double2* s0 = reinterpret_cast<const double2*>(in + c * cstride + row0 * pitch);
+    const double2* s1 = reinterpret_cast<const double2*>(in + c * cstride + (row0 + 1) * pitch);
+    double2 a[16], b[16], v[32];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {   // packed pairs (x[2n], x[2n+1]), n < 256 non-zero
+        a[m] = m < 8 ? __ldg(s0 + lane + 32 * m) : make_double2(0.0, 0.0);
+        b[m] = m < 8 ? __ldg(s1 + lane + 32 * m) : make_double2(0.0, 0.0);
+    }
+    fw::fft512x2<-1>(a, b, v, Wc, lane, tw512);
+    // Z_line[k1 + 16 k2] -> tile, natural order per line
+    const int line = lane >> 4, k1 = lane & 15;
+    __syncwarp();
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) Wc[line * XM + k1 + 16 * k2] = v[fw::p32(k2)];
+    __syncwarp();
+    for (int base = 0; base < XHX; base += XCHUNK) {
+        const int cnt = XHX - base < XCHUNK ? XHX - base : XCHUNK;
+        for (int it = lane; it < 2 * cnt; it += 32) {
+            const int ln = it / cnt, kx = base + (it - ln * cnt);
+            const double2 zk = Wc[ln * XM + (kx & (XM - 1))];
+            const double2 zm = Wc[ln * XM + ((XM - kx) & (XM - 1))];
+            // E = (Zk + conj Zm)/2, O = (Zk - conj Zm)/(2i), X = E + W^k O
+            const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+            const double2 Od = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+            O[(ln * XCHUNK + (kx - base)) * 3 + c] = cadd(E, cmul(tw1024[kx], Od));
+        }
+        __syncthreads();
+        if (PM) {
+            // out[kx][row][c]: the pair's 6 values per bin are contiguous
+            for (int j = threadIdx.x; j < cnt * 6; j += 96) {
+                const int kr = j / 6, r = j - 6 * kr, ln = r / 3, cc = r - 3 * ln;
+                out[(long long)(base + kr) * BLKE + (row0 + ln) * 3 + cc] = O[(ln * XCHUNK + kr) * 3 + cc];
+            }
+        } else {
+            // out[row][kx][c]: cnt * 3 contiguous values per row
+            for (int j = threadIdx.x; j < cnt * 6; j += 96) {
+                const int ln = j / (cnt * 3), r = j - ln * cnt * 3;
+                out[((row0 + ln) * CHP + base) * 3 + r] = O[ln * XCHUNK * 3 + r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <bool PM>
+__global__ void __launch_bounds__(96, 4)
+k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restrict__ out, long long cstride,
+        int pitch, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
+        const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    extern __shared__ double2 S[];                 // [line][kx][c] input pair, then 3 x 1024 tiles
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long row0 = 2LL * blockIdx.x;
+    if (PM) {
+        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
+            const int kx = j / 6, r = j - 6 * kx, ln = r / 3, cc = r - 3 * ln;
+            cp_async16(&S[(ln * XHX + kx) * 3 + cc], X + (long long)kx * BLKE + (row0 + ln) * 3 + cc, true);
+        }
+    } else {
+        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
+            const int ln = j / (XHX * 3), r = j - ln * XHX * 3;
+            cp_async16(&S[ln * XHX * 3 + r], X + (row0 + ln) * CHP * 3 + r, true);
+        }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    double2 a[16], b[16], v[32];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int k = lane + 32 * m;
+        const double2 w = tw1024[k];
+#pragma unroll
+        for (int ln = 0; ln < 2; ++ln) {
+            const double2 xk = S[(ln * XHX + k) * 3 + c];
+            const double2 xm = S[(ln * XHX + (XM - k)) * 3 + c];
+            // Z = (Xk + conj Xm) + i (Xk - conj Xm) W^-k
+            const double2 A = make_double2(xk.x + xm.x, xk.y - xm.y);
+            const double2 Bm = make_double2(xk.x - xm.x, xk.y + xm.y);
+            const double2 B = cmul(Bm, make_double2(w.x, -w.y));
+            const double2 z = make_double2(A.x - B.y, A.y + B.x);
+            if (ln == 0) a[m] = z; else b[m] = z;
+        }
+    }
+    __syncthreads();   // S becomes the transpose tiles
+    fw::fft512x2<1>(a, b, v, S + c * 1024, lane, tw512);
+    const int line = lane >> 4, k1 = lane & 15;
+    double2* dst = reinterpret_cast<double2*>(out + c * cstride + (row0 + line) * pitch);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) dst[k1 + 16 * k2] = v[fw::p32(k2)];   // n < 256: x[2n], x[2n+1]
+}
+
+// -1 when the shape is not covered (the radix-16 kernels take it)
+int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, long long cstride, int pitch,
+              int nhalf, int CH, int CHP, long long BLKE, long long nrows, const double2* twM,
+              const double2* tw2M, cudaStream_t st, const int* halt) {
+    const char* xe = getenv("MXB_XWARP");
+    const bool on = !(xe && xe[0] == '0');
+    if (!on || M != XM || nhalf != XM / 2 || (nrows & 1) || pitch != XM) return -1;
+    const bool pm = CH == 1;
+    if (!pm && CH < XHX) return -1;   // row-major only for a single rank
+    const unsigned grid = (unsigned)(nrows / 2);
+    const size_t smem_r2c = (size_t)3 * 1024 * sizeof(double2);
+    const size_t smem_c2r = (size_t)2 * XHX * 3 * sizeof(double2);   // >= the tiles
+    static bool attrs = false;
+    if (!attrs) {
+        MXB_CUDA(cudaFuncSetAttribute(k_r2c_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r2c));
+        MXB_CUDA(cudaFuncSetAttribute(k_r2c_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r2c));
+        MXB_CUDA(cudaFuncSetAttribute(k_c2r_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c2r));
+        MXB_CUDA(cudaFuncSetAttribute(k_c2r_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c2r));
+        for (const void* f : {(const void*)k_r2c_w<true>, (const void*)k_r2c_w<false>, (const void*)k_c2r_w<true>,
+                              (const void*)k_c2r_w<false>})
+            MXB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attrs = true;
+    }
+    if (fwd) {
+        if (pm) k_r2c_w<true><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt);
+        else k_r2c_w<false><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt);
+    } else {
+        if (pm) k_c2r_w<true><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt);
+        else k_c2r_w<false><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt);
+    }
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+}  // namespace mxb
