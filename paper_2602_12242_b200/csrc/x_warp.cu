@@ -24,17 +24,15 @@ using namespace ff;
 namespace {
 constexpr int XM = 512;          // complex FFT length (px / 2)
 constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
-constexpr int XCHUNK = 128;      // r2c output staging chunk (bins)
 }
 
 template <bool PM>
-__global__ void __launch_bounds__(96, 3)
+__global__ void __launch_bounds__(96, 4)
 k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __restrict__ out, int CHP,
         long long BLKE, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
         const int* __restrict__ halt) {
     if (halt && *halt) return;
-    extern __shared__ double2 W[];                 // 3 x 1024 transpose tiles
-    __shared__ double2 O[2 * XCHUNK * 3];          // [line][bin][c] output chunk
+    extern __shared__ double2 W[];   // 3 x 1024 transpose tiles, then the [line][kx][c] output pair
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * 1024;
     const long long row0 = 2LL * blockIdx.x;
@@ -48,37 +46,51 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
     }
     fw::fft512x2<-1>(a, b, v, Wc, lane, tw512);
     // Z_line[k1 + 16 k2] -> tile, natural order per line
-    const int line = lane >> 4, k1 = lane & 15;
-    __syncwarp();
+    {
+        const int line = lane >> 4, k1 = lane & 15;
+        __syncwarp();
 #pragma unroll
-    for (int k2 = 0; k2 < 32; ++k2) Wc[line * XM + k1 + 16 * k2] = v[fw::p32(k2)];
-    __syncwarp();
-    for (int base = 0; base < XHX; base += XCHUNK) {
-        const int cnt = XHX - base < XCHUNK ? XHX - base : XCHUNK;
-        for (int it = lane; it < 2 * cnt; it += 32) {
-            const int ln = it / cnt, kx = base + (it - ln * cnt);
-            const double2 zk = Wc[ln * XM + (kx & (XM - 1))];
-            const double2 zm = Wc[ln * XM + ((XM - kx) & (XM - 1))];
-            // E = (Zk + conj Zm)/2, O = (Zk - conj Zm)/(2i), X = E + W^k O
-            const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-            const double2 Od = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-            O[(ln * XCHUNK + (kx - base)) * 3 + c] = cadd(E, cmul(tw1024[kx], Od));
-        }
-        __syncthreads();
-        if (PM) {
-            // out[kx][row][c]: the pair's 6 values per bin are contiguous
-            for (int j = threadIdx.x; j < cnt * 6; j += 96) {
-                const int kr = j / 6, r = j - 6 * kr, ln = r / 3, cc = r - 3 * ln;
-                out[(long long)(base + kr) * BLKE + (row0 + ln) * 3 + cc] = O[(ln * XCHUNK + kr) * 3 + cc];
-            }
-        } else {
-            // out[row][kx][c]: cnt * 3 contiguous values per row
-            for (int j = threadIdx.x; j < cnt * 6; j += 96) {
-                const int ln = j / (cnt * 3), r = j - ln * cnt * 3;
-                out[((row0 + ln) * CHP + base) * 3 + r] = O[ln * XCHUNK * 3 + r];
+        for (int k2 = 0; k2 < 32; ++k2) Wc[line * XM + k1 + 16 * k2] = v[fw::p32(k2)];
+        __syncwarp();
+    }
+    // untangle all XHX bins of both lines into registers (bin kx = lane + 32 i)
+    constexpr int NI = (XHX + 31) / 32;   // 17
+    double2 xo[2][NI];
+#pragma unroll
+    for (int ln = 0; ln < 2; ++ln)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int kx = lane + 32 * i;
+            if (kx < XHX) {
+                const double2 zk = Wc[ln * XM + (kx & (XM - 1))];
+                const double2 zm = Wc[ln * XM + ((XM - kx) & (XM - 1))];
+                // E = (Zk + conj Zm)/2, O = (Zk - conj Zm)/(2i), X = E + W^k O
+                const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+                const double2 Od = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+                xo[ln][i] = cadd(E, cmul(tw1024[kx], Od));
             }
         }
-        __syncthreads();
+    __syncthreads();   // every warp is done with its tile: stage [line][kx][c]
+#pragma unroll
+    for (int ln = 0; ln < 2; ++ln)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int kx = lane + 32 * i;
+            if (kx < XHX) W[(ln * XHX + kx) * 3 + c] = xo[ln][i];
+        }
+    __syncthreads();
+    if (PM) {
+        // out[kx][row][c]: the pair's 6 values per bin are contiguous
+        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
+            const int kx = j / 6, r = j - 6 * kx, ln = r / 3, cc = r - 3 * ln;
+            out[(long long)kx * BLKE + (row0 + ln) * 3 + cc] = W[(ln * XHX + kx) * 3 + cc];
+        }
+    } else {
+        // out[row][kx][c]: XHX * 3 contiguous values per row
+        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
+            const int ln = j / (XHX * 3), r = j - ln * XHX * 3;
+            out[((row0 + ln) * CHP) * 3 + r] = W[ln * XHX * 3 + r];
+        }
     }
 }
 
@@ -140,7 +152,7 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
     const bool pm = CH == 1;
     if (!pm && CH < XHX) return -1;   // row-major only for a single rank
     const unsigned grid = (unsigned)(nrows / 2);
-    const size_t smem_r2c = (size_t)3 * 1024 * sizeof(double2);
+    const size_t smem_r2c = (size_t)2 * XHX * 3 * sizeof(double2);   // >= the tiles
     const size_t smem_c2r = (size_t)2 * XHX * 3 * sizeof(double2);   // >= the tiles
     static bool attrs = false;
     if (!attrs) {
