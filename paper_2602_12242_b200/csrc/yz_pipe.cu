@@ -482,6 +482,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + (size_t)j * 128) : "memory");
         }
 #endif
+        // one forward FFT instance (A, B: zero-padded inputs) and one inverse
+        // instance (B, C: half of the outputs kept) -- four inlined FFT bodies
+        // overflowed the instruction cache
         double2 v[32];
         if (cur.kind == U_C) {
 #pragma unroll
@@ -491,79 +494,80 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             for (int m = 0; m < 32; ++m) v[m] = m < 16 ? W[(lane + 32 * m) * 3 + c] : make_double2(0.0, 0.0);
         }
         __syncthreads();   // W becomes the transpose tiles
-
-        if (cur.kind == U_A) {
-            // ---- y forward of row z = idx -> slot row [ky][c]
+        bool inverse = cur.kind == U_C;
+        if (cur.kind != U_C) {
             fw::fft1024<-1>(v, Wc, lane, tw);
             if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            if (cur.kind == U_A) {
+                // ---- y forward of row z = idx -> slot row [ky][c]
 #if MXB_PIPE_W_DIRECT_STORE
-            {
                 double2* dst = slot + (long long)cur.idx * L * 3 + c;
 #pragma unroll
                 for (int k = 0; k < 32; ++k) st_l2(dst + (long long)(lane + 32 * k) * 3, v[fw::p32(k)]);
-            }
 #else
-            store_rows(v, std::integral_constant<int, 32>{}, slot + (long long)cur.idx * L * 3, L, false, lane);
+                store_rows(v, std::integral_constant<int, 32>{}, slot + (long long)cur.idx * L * 3, L, false, lane);
 #endif
-        } else if (cur.kind == U_B) {
-            // ---- z forward * K * z inverse of column ky = idx
-            const int ky = cur.idx;
-            fw::fft1024<-1>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
-            __syncwarp();
+            } else {
+                // ---- B: * K between the z forward and z inverse of column ky = idx
+                const int ky = cur.idx;
+                __syncwarp();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) Wc[lane + 32 * k] = v[fw::p32(k)];
-            __syncthreads();
-            const bool fy = 2 * ky > L;
-            const double s = a.scale;
-            // each thread owns whole kz rows (all 3 components), in place in W
-            for (int kz = threadIdx.x; kz < L; kz += 96) {
-                const bool fz = 2 * kz > L;
-                const double2* kr = KS + (fz ? L - kz : kz) * 3;
-                const double2 q01 = kr[0], q23 = kr[1], q45 = kr[2];
-                const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
-                const double kxy = fy ? -q01.y : q01.y;
-                const double kxz = fz ? -q23.x : q23.x;
-                const double kyz = (fy != fz) ? -q45.x : q45.x;
-                const double2 m0 = W[kz], m1 = W[L + kz], m2 = W[2 * L + kz];
-                const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
-                                                kxx * m0.y + kxy * m1.y + kxz * m2.y);
-                const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
-                                                kxy * m0.y + kyy * m1.y + kyz * m2.y);
-                const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
-                                                kxz * m0.y + kyz * m1.y + kzz * m2.y);
-                W[kz] = make_double2(h0.x * s, h0.y * s);
-                W[L + kz] = make_double2(h1.x * s, h1.y * s);
-                W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
+                for (int k = 0; k < 32; ++k) Wc[lane + 32 * k] = v[fw::p32(k)];
+                __syncthreads();
+                const bool fy = 2 * ky > L;
+                const double s = a.scale;
+                // each thread owns whole kz rows (all 3 components), in place in W
+                for (int kz = threadIdx.x; kz < L; kz += 96) {
+                    const bool fz = 2 * kz > L;
+                    const double2* kr = KS + (fz ? L - kz : kz) * 3;
+                    const double2 q01 = kr[0], q23 = kr[1], q45 = kr[2];
+                    const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                    const double kxy = fy ? -q01.y : q01.y;
+                    const double kxz = fz ? -q23.x : q23.x;
+                    const double kyz = (fy != fz) ? -q45.x : q45.x;
+                    const double2 m0 = W[kz], m1 = W[L + kz], m2 = W[2 * L + kz];
+                    const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                    kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                    const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                    kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                    const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                    kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                    W[kz] = make_double2(h0.x * s, h0.y * s);
+                    W[L + kz] = make_double2(h1.x * s, h1.y * s);
+                    W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
+                }
+                __syncthreads();
+#pragma unroll
+                for (int m = 0; m < 32; ++m) v[m] = Wc[lane + 32 * m];
+                __syncthreads();   // all reads of W done before the tiles are reused
+                inverse = true;
             }
-            __syncthreads();
-#pragma unroll
-            for (int m = 0; m < 32; ++m) v[m] = Wc[lane + 32 * m];
-            __syncthreads();   // all reads of W done before the tiles are reused
+        }
+        if (inverse) {
             fw::fft1024<1>(v, Wc, lane, tw);
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < 16; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
-            __syncthreads();
-            double2* col = slot + (long long)ky * 3;
-            for (int j = threadIdx.x; j < 3 * N; j += 96) {
-                const int z = j / 3, cc = j - 3 * z;
-                st_l2(col + (long long)z * L * 3 + cc, W[j]);
-            }
-        } else {
-            // ---- y inverse of row z = idx -> XP row (n of L kept)
-            fw::fft1024<1>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            if (cur.kind == U_C) {
+                // ---- y inverse of row z = idx -> XP row (n of L kept)
+                if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
 #if MXB_PIPE_W_DIRECT_STORE
-            {
                 double2* dst = a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3 + c;
 #pragma unroll
                 for (int k = 0; k < 16; ++k) st_stream(dst + (long long)(lane + 32 * k) * 3, v[fw::p32(k)]);
-            }
 #else
-            store_rows(v, std::integral_constant<int, 16>{}, a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3,
-                       N, true, lane);
+                store_rows(v, std::integral_constant<int, 16>{}, a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3,
+                           N, true, lane);
 #endif
+            } else {
+                // ---- B: the first n of the inverse column back into the slot
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 16; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
+                __syncthreads();
+                double2* col = slot + (long long)cur.idx * 3;
+                for (int j = threadIdx.x; j < 3 * N; j += 96) {
+                    const int z = j / 3, cc = j - 3 * z;
+                    st_l2(col + (long long)z * L * 3 + cc, W[j]);
+                }
+            }
         }
         __syncthreads();
         pending = cur;
