@@ -42,7 +42,7 @@
 #include "fft_warp.cuh"
 
 #ifndef MXB_PIPE_W_CTAS
-#define MXB_PIPE_W_CTAS 3
+#define MXB_PIPE_W_CTAS 4
 #endif
 #ifndef MXB_PIPE_DISCARD
 #define MXB_PIPE_DISCARD 1
@@ -401,10 +401,12 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
 
 // ---------------------------------------------------------------------------
 // warp-FFT variant, L = 1024 (n = 512): one line per warp (fft_warp.cuh), the
-// CTA is the component triple.  W (3 x 1024) first stages the unit's lines
-// (cp.async, natural [e][3] layout), then serves as the three warps'
-// transpose tiles; KS holds a B unit's kernel rows.  Zero-padded halves
-// (A/B inputs, B/C outputs) are compile-time and fold away.
+// CTA is the component triple.  W (3 x 1024 = 48 KB) first stages the unit's
+// lines (cp.async, natural [e][3] layout), then serves as the three warps'
+// transpose tiles and B's component exchange; B reads its kernel rows through
+// the read-only path.  48 KB and 168 registers give four CTAs (12 warps) per
+// SM.  Zero-padded halves (A/B inputs, B/C outputs) are compile-time and fold
+// away.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(96, MXB_PIPE_W_CTAS)
 k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
@@ -414,7 +416,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     __shared__ long long next_ticket;
     __shared__ int flag;
     double2* W = sm;                                        // 3 x 1024
-    const double2* KS = sm + 3 * L;                         // L2 x 3 (6 doubles per kz')
+    // kernel rows are read through the read-only path in the multiply (a
+    // warp's 32 consecutive kz rows are 1.5 KB contiguous)
+    const double2* __restrict__ Kp2 = reinterpret_cast<const double2*>(a.Kp);
     const int hx = a.hx;
     const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -433,9 +437,6 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 const int z = j / 3, cc = j - 3 * z;
                 cp_async16(&W[j], col + (long long)z * L * 3 + cc, true);
             }
-            const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
-            const double2* ks = reinterpret_cast<const double2*>(a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6);
-            for (int j = threadIdx.x; j < 3 * L2; j += 96) cp_async16(const_cast<double2*>(KS) + j, ks + j, true);
         } else {
             const double2* src = slot + (long long)u.idx * L * 3;
             for (int j = threadIdx.x; j < 3 * L; j += 96) cp_async16(&W[j], src + j, true);
@@ -516,11 +517,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 __syncthreads();
                 const bool fy = 2 * ky > L;
                 const double s = a.scale;
+                const double2* krow = Kp2 + ((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 * 3;
                 // each thread owns whole kz rows (all 3 components), in place in W
                 for (int kz = threadIdx.x; kz < L; kz += 96) {
                     const bool fz = 2 * kz > L;
-                    const double2* kr = KS + (fz ? L - kz : kz) * 3;
-                    const double2 q01 = kr[0], q23 = kr[1], q45 = kr[2];
+                    const double2* kr = krow + (fz ? L - kz : kz) * 3;
+                    const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
                     const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
                     const double kxy = fy ? -q01.y : q01.y;
                     const double kxz = fz ? -q23.x : q23.x;
@@ -629,7 +631,7 @@ bool pipe_shape_ok(int ny, int nz) {
 }
 
 static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
-    const size_t smem = (size_t)(3 * 1024 + 3 * 513) * sizeof(double2);
+    const size_t smem = (size_t)(3 * 1024) * sizeof(double2);
     static int grid = 0;
     if (!grid) {
         MXB_CUDA(cudaFuncSetAttribute(k_yz_pipe_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
