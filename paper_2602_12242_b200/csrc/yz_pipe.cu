@@ -437,6 +437,13 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 const int z = j / 3, cc = j - 3 * z;
                 cp_async16(&W[j], col + (long long)z * L * 3 + cc, true);
             }
+            if (threadIdx.x == 0) {
+                // pull the unit's kernel row (L2 x 48 B) into L2 over the forward FFT;
+                // the multiply reads it through the read-only path
+                const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
+                const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+            }
         } else {
             const double2* src = slot + (long long)u.idx * L * 3;
             for (int j = threadIdx.x; j < 3 * L; j += 96) cp_async16(&W[j], src + j, true);
