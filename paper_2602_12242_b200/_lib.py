@@ -12,7 +12,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmagnex_b200.so")
+# MXB_LIB: load another build of the same ABI (variant experiments, tools/build_variant.py)
+LIB_PATH = os.environ.get("MXB_LIB") or os.path.join(HERE, "libmagnex_b200.so")
 
 OK, EINVAL, EDEAD, EBLOWUP, ECUDA, ENCCL, EQUILIBRATED = 0, 1, 2, 3, 4, 5, 6
 TERM_EXCHANGE, TERM_ANISOTROPY, TERM_DMI, TERM_DEMAG, TERM_BIAS, TERM_CUBIC, TERM_BULK_DMI = (

@@ -260,7 +260,8 @@ __device__ __forceinline__ void heff_nb(const StageArgs& a, const double* f, lon
                                         uint32_t terms, const double xp[3], const double xm[3],
                                         const double yp[3], const double ym[3], const double zp[3],
                                         const double zm[3], double fxp, double fxm, double fyp,
-                                        double fym, double fzp, double fzm, double h[3]);
+                                        double fym, double fzp, double fzm, double h[3],
+                                        const double* hd_pre = nullptr);
 
 // H_eff of one cell in the reference accumulation order.
 template <bool E, bool U>
@@ -301,7 +302,8 @@ __device__ __forceinline__ void heff_nb(const StageArgs& a, const double* f, lon
                                         uint32_t terms, const double xp[3], const double xm[3],
                                         const double yp[3], const double ym[3], const double zp[3],
                                         const double zm[3], double fxp, double fxm, double fyp,
-                                        double fym, double fzp, double fzm, double h[3]) {
+                                        double fym, double fzp, double fzm, double h[3],
+                                        const double* hd_pre) {
     const Grid& g = a.g;
     h[0] = 0.0; h[1] = 0.0; h[2] = 0.0;
     const bool ex = terms & MXB_TERM_EXCHANGE;
@@ -390,9 +392,9 @@ __device__ __forceinline__ void heff_nb(const StageArgs& a, const double* f, lon
     }
     if (terms & MXB_TERM_DEMAG) {
         const long long N = g.N;
-        h[0] = add<E>(h[0], ld(a.hd, idx));
-        h[1] = add<E>(h[1], ld(a.hd, N + idx));
-        h[2] = add<E>(h[2], ld(a.hd, 2 * N + idx));
+        h[0] = add<E>(h[0], hd_pre ? hd_pre[0] : ld(a.hd, idx));
+        h[1] = add<E>(h[1], hd_pre ? hd_pre[1] : ld(a.hd, N + idx));
+        h[2] = add<E>(h[2], hd_pre ? hd_pre[2] : ld(a.hd, 2 * N + idx));
     }
     if (terms & MXB_TERM_BIAS) {
         double b0 = a.bias[0], b1 = a.bias[1], b2 = a.bias[2];
@@ -498,7 +500,8 @@ __device__ void reduce_partials(const double* partials, int nblk, const bool is_
 // accumulates the step partials for the final RK4 / Euler stage)
 template <int MODE, bool E>
 __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, const CellMat& cm,
-                                           const double m[3], const double h[3], double red[4]) {
+                                           const double m[3], const double h[3], double red[4],
+                                           const double* y_pre = nullptr) {
     const long long N = a.g.N;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
         if (MODE == M_HEFF) {
@@ -509,7 +512,8 @@ __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, co
         if (MODE == M_RHS) {
             a.out[idx] = kk[0]; a.out[N + idx] = kk[1]; a.out[2 * N + idx] = kk[2];
         } else {
-            const double y[3] = {ld(a.y, idx), ld(a.y, N + idx), ld(a.y, 2 * N + idx)};
+            const double y[3] = {y_pre ? y_pre[0] : ld(a.y, idx), y_pre ? y_pre[1] : ld(a.y, N + idx),
+                                 y_pre ? y_pre[2] : ld(a.y, 2 * N + idx)};
             double v[3];
             if (MODE == M_RK1 || MODE == M_RK2 || MODE == M_RK3 || MODE == M_EULER) {
 #pragma unroll
@@ -687,7 +691,19 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
 // tile with a one-cell halo ring, z neighbours stay in registers.  Same
 // neighbour values, face coefficients and arithmetic as k_stage.
 // ---------------------------------------------------------------------------
-constexpr int ZTX = 32, ZTY = 8, ZC = 16;
+#ifndef MXB_ZTY
+#define MXB_ZTY 8
+#endif
+#ifndef MXB_ZC
+#define MXB_ZC 16
+#endif
+#ifndef MXB_ZM_CTAS
+#define MXB_ZM_CTAS 3
+#endif
+#ifndef MXB_ZM_PRELOAD_Y
+#define MXB_ZM_PRELOAD_Y 0
+#endif
+constexpr int ZTX = 32, ZTY = MXB_ZTY, ZC = MXB_ZC;
 
 template <bool E>
 __device__ __forceinline__ void ghost_nb(const StageArgs& a, int axis, int step, const double m[3],
@@ -710,7 +726,7 @@ __device__ __forceinline__ void ghost_nb(const StageArgs& a, int axis, int step,
 }
 
 template <int MODE, bool E>
-__global__ void __launch_bounds__(256, 3) k_stage_zm(StageArgs a) {
+__global__ void __launch_bounds__(ZTX * ZTY, MXB_ZM_CTAS) k_stage_zm(StageArgs a) {
     if (a.halt && *(volatile const int*)a.halt) return;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
     __shared__ double tile[3][ZTY + 2][ZTX + 2];
@@ -740,8 +756,21 @@ __global__ void __launch_bounds__(256, 3) k_stage_zm(StageArgs a) {
     load(k0, zcv);
     bool zm_ok = load(k0 - 1, zmv);
     const bool ex = a.terms & MXB_TERM_EXCHANGE;
+    const bool kHd = (a.terms & MXB_TERM_DEMAG) && a.hd;
+    constexpr bool kY = MXB_ZM_PRELOAD_Y && MODE >= M_RK1;
     for (int k = k0; k < k1; ++k) {
         const bool zp_ok = load(k + 1, zpv);
+        // this plane's demag field (and step-start state) issued before the
+        // barriers and the tile fill, so their latency overlaps them
+        double hdv[3] = {0.0, 0.0, 0.0}, yv[3] = {0.0, 0.0, 0.0};
+        if (in) {
+            const long long o = (long long)k * plane + col;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (kHd) hdv[q] = ld(a.hd, q * N + o);
+                if (kY) yv[q] = ld(a.y, q * N + o);
+            }
+        }
         __syncthreads();
         if (in) {
             const long long o = (long long)k * plane + col;
@@ -780,8 +809,8 @@ __global__ void __launch_bounds__(256, 3) k_stage_zm(StageArgs a) {
             (void)ex;
             heff_nb<E, true>(a, f, idx, i, j, k, m, cm, a.terms, xp, xm, yp, ym, zp, zm,
                              okxp ? hf : A, okxm ? hf : A, okyp ? hf : A, okym ? hf : A,
-                             zp_ok ? hf : A, zm_ok ? hf : A, h);
-            stage_tail<MODE, E>(a, idx, cm, m, h, red);
+                             zp_ok ? hf : A, zm_ok ? hf : A, h, kHd ? hdv : nullptr);
+            stage_tail<MODE, E>(a, idx, cm, m, h, red, kY ? yv : nullptr);
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q) { zmv[q] = zcv[q]; zcv[q] = zpv[q]; }
@@ -818,8 +847,8 @@ int stage_nparts(const StageArgs& a) {
 
 template <int MODE>
 static void launch_zm(bool exact, const StageArgs& a, cudaStream_t st) {
-    if (exact) k_stage_zm<MODE, true><<<zm_grid(a.g), kBlock, 0, st>>>(a);
-    else k_stage_zm<MODE, false><<<zm_grid(a.g), kBlock, 0, st>>>(a);
+    if (exact) k_stage_zm<MODE, true><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
+    else k_stage_zm<MODE, false><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
 }
 
 template <int MODE, bool E>
