@@ -827,14 +827,19 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZM_CTAS) k_stage_zm(StageArgs a
     }
 }
 
-static bool zm_eligible(const StageArgs& a) {
-    static const bool on = getenv("MXB_ZMARCH") == nullptr || atoi(getenv("MXB_ZMARCH")) != 0;
-    return on && a.mat.uniform && a.mat.all_magnetic && a.ghost != MXB_GHOST_PERIODIC &&
-           !(a.terms & (MXB_TERM_CUBIC | MXB_TERM_BULK_DMI)) && (long long)a.g.nx * a.g.ny >= 256;
-}
-
 static dim3 zm_grid(const Grid& g) {
     return dim3((g.nx + ZTX - 1) / ZTX, (g.ny + ZTY - 1) / ZTY, (g.nz + ZC - 1) / ZC);
+}
+
+// the z-marching kernel needs enough column tiles to fill the GPU (at 32^3 it
+// would run 8 CTAs); small grids take the one-cell-per-thread kernel
+static bool zm_eligible(const StageArgs& a) {
+    static const bool on = getenv("MXB_ZMARCH") == nullptr || atoi(getenv("MXB_ZMARCH")) != 0;
+    if (!(on && a.mat.uniform && a.mat.all_magnetic && a.ghost != MXB_GHOST_PERIODIC &&
+          !(a.terms & (MXB_TERM_CUBIC | MXB_TERM_BULK_DMI)) && (long long)a.g.nx * a.g.ny >= 256))
+        return false;
+    const dim3 gz = zm_grid(a.g);
+    return (long long)gz.x * gz.y * gz.z >= 4 * 148;
 }
 
 int stage_nparts(const StageArgs& a) {
