@@ -232,13 +232,15 @@ def run_slab(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--size", type=int, default=512, help="cells per edge of the synthetic cube")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-n", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="timed runs of --steps steps; the median is reported (SURVEY 8d)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="collectives for N > 1 (gloo only to exercise the path on one GPU)")
     args = ap.parse_args()
@@ -286,10 +288,15 @@ def main():
     # warm-up
     L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, max(args.warmup, 1), bptr,
                      C.byref(ms_tot), None, C.byref(nl)))
+    runs, runs_st = [], []
     with Clocks(local) as clk:
-        L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, args.steps, bptr,
-                         C.byref(ms_tot), C.byref(ms_st), C.byref(nl)))
-    t_step = ms_tot.value / args.steps
+        for _ in range(max(args.repeats, 1)):
+            L.check(ctx.call("mxb_time_steps", d, C.byref(ts), dt, args.steps, bptr,
+                             C.byref(ms_tot), C.byref(ms_st), C.byref(nl)))
+            runs.append(ms_tot.value / args.steps)
+            runs_st.append(ms_st.value / args.steps)
+    t_step = float(np.median(runs))
+    ms_st = C.c_double(float(np.median(runs_st)) * args.steps)
     value = N / (t_step * 1e-3)
     # per-kernel timing for the roofline
     ms_eval = C.c_double()
@@ -367,6 +374,8 @@ def main():
                           "achieved_GBs": step_bytes / (t_step * 1e-3) / 1e9,
                           "frac": step_bytes / (t_step * 1e-3) / 1e9 / hbm},
         "kernels_ms_per_step": share,
+        "timing": {"repeats": len(runs), "ms_per_step_runs": runs, "statistic": "median",
+                   "clock": "CUDA events on the solver stream"},
         "demag_ms_per_eval": ms_eval.value, "cufft_demag_ms_per_eval": ms_cufft.value,
         "tensor_build_s": t_build,
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(nl.value),
