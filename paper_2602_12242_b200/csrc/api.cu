@@ -478,7 +478,7 @@ int mxb_demag_field(mxb_demag* d, const double* m, double* h) {
     if (rc) return rc;
     MXB_CUDA(cudaMemcpyAsync(h, d->io[1], b, cudaMemcpyDeviceToHost, d->st));
     MXB_CUDA(cudaStreamSynchronize(d->st));
-    return MXB_OK;
+    return p.check_abort();
 }
 
 // ---------------------------------------------------------------------------
@@ -569,7 +569,8 @@ static int heff_common(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_b
     a.ys = c->tA;
     a.out = c->tB;
     if ((rc = launch_stage(mode, c->exact, a, c->st))) return rc;
-    return download_out(c, out);
+    if ((rc = download_out(c, out))) return rc;
+    return (t->mask & MXB_TERM_DEMAG) && d ? d->plan.check_abort() : MXB_OK;
 }
 
 int mxb_heff(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_bias* b, const double* m,
@@ -655,7 +656,7 @@ static int energies_dev(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_
     MXB_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st));
     MXB_CUDA(cudaStreamSynchronize(c->st));
     for (int q = 0; q < 4; ++q) out[q] = h.energies[q];
-    return MXB_OK;
+    return (t->mask & MXB_TERM_DEMAG) && d ? d->plan.check_abort() : MXB_OK;
 }
 
 int mxb_energies(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_bias* b,
@@ -1043,6 +1044,10 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     st->status = h.halt;
     if (h.halt == MXB_EBLOWUP) { set_error("integration blew up"); return MXB_EBLOWUP; }
     if (h.halt == MXB_EDEAD) { set_error("magnetic cell with |M| = 0"); return MXB_EDEAD; }
+    if (h.halt == MXB_ECUDA) {
+        set_error("demag plane pipeline: dependency wait timed out (scheduling fault)");
+        return MXB_ECUDA;
+    }
     return MXB_OK;
 }
 

@@ -622,6 +622,17 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
     return MXB_OK;
 }
 
+int DemagPlan::check_abort() {
+    if (!pipe || !bar) return MXB_OK;
+    unsigned w = 0;
+    MXB_CUDA(cudaMemcpy(&w, bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    if (w) {
+        set_error("demag plane pipeline: dependency wait timed out (scheduling fault); field invalid");
+        return MXB_ECUDA;
+    }
+    return MXB_OK;
+}
+
 int DemagPlan::field_dev(const double* m, double* h, cudaStream_t st, const int* halt,
                          cudaEvent_t* ev) {
     if (G != 1) { set_error("field_dev is the single-rank pipeline"); return MXB_EINVAL; }

@@ -84,6 +84,9 @@ struct DemagPlan {
     int x_forward(const double* m_local, cudaStream_t st, const int* halt);
     int yz(cudaStream_t st, const int* halt, cudaEvent_t* ev = nullptr);
     int x_inverse(double* h_local, cudaStream_t st, const int* halt);
+    // after a synchronised plane-pipeline evaluation: MXB_ECUDA if its
+    // dependency guard fired (the field is then invalid)
+    int check_abort();
 };
 
 int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);

@@ -146,7 +146,9 @@ struct Sched {
     // across the unit loop of the FFT kernels)
     unsigned* base;
     int hx, n, L;
-    __device__ Sched(const PipeArgs& a, int L_) : base(a.sync), hx(a.hx), n(a.n), L(L_) {}
+    int* halt;   // the run's halt word (null for a direct field evaluation)
+    __device__ Sched(const PipeArgs& a, int L_, const int* halt_) :
+        base(a.sync), hx(a.hx), n(a.n), L(L_), halt(const_cast<int*>(halt_)) {}
     __device__ unsigned* ticket() const { return base; }
     __device__ unsigned* abort_w() const { return base + 1; }
     __device__ unsigned* doneA() const { return base + 2; }
@@ -205,6 +207,9 @@ struct Sched {
                         printf("k_yz_pipe: wait timeout cta %d kind %d plane %d idx %d have %u need %u\n",
                                blockIdx.x, u.kind, u.plane, u.idx, ld_acquire(c), tg);
                         atomicExch(abort_w(), 1u);
+                        // the run loop stops with MXB_ECUDA; a direct evaluation
+                        // reports it from the abort word (DemagPlan::check_abort)
+                        if (halt) atomicExch(halt, (int)MXB_ECUDA);
                         *flag = 0;
                         break;
                     }
@@ -239,7 +244,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     const long long plane_xp = (long long)n * n * 3;       // XP elements per kx plane
     const long long slot_e = (long long)n * L * 3;         // slot elements
     const int b = threadIdx.x / TPL, t = threadIdx.x - (threadIdx.x / TPL) * TPL;
-    const Sched sc(a, L);
+    const Sched sc(a, L, halt);
     const TicketMap tmap{hx, n, L};
 
     // unit inputs, staged in S with cp.async: A an XP row (HBM), B a slot
@@ -423,7 +428,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * L;
-    const Sched sc(a, L);
+    const Sched sc(a, L, halt);
     const TicketMap tmap{hx, N, L};
 
     auto stage = [&](const Unit& u) {
