@@ -1210,7 +1210,7 @@ int mxb_time_steps(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, double dt, int 
         cudaEventElapsedTime(&ms, e0, e1);
         *ms_stencil = ms;
     }
-    if (launches) *launches = (int64_t)nsteps * (4 * (use_demag ? 6 : 1) + 1);
+    if (launches) *launches = (int64_t)nsteps * (4 * (1 + (use_demag ? d->plan.kernels_per_eval() : 0)) + 1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return MXB_OK;

@@ -87,6 +87,8 @@ struct DemagPlan {
     // after a synchronised plane-pipeline evaluation: MXB_ECUDA if its
     // dependency guard fired (the field is then invalid)
     int check_abort();
+    // kernels one evaluation launches: x forward, the y/z part, x inverse
+    int kernels_per_eval() const { return pipe ? 3 : (pz > 1 && py > 1 ? 5 : 3); }
 };
 
 int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);
