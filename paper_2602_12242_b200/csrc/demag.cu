@@ -368,9 +368,9 @@ bool DemagPlan::pipe_candidate() const {
     const char* e = getenv("MXB_PIPE");
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return true;
-    // measured on B200: on par with the 5-pass path at L = 1024 (and 13 GB less
-    // HBM at 512^3), slower below; see DESIGN.md
-    return pz >= 1024;
+    // measured on B200 with the warp-FFT pipelines: 23.9 vs 34.4 ms for the y/z
+    // part at 512^3 (L = 1024), 4.03 vs 4.55 ms at 256^3 (L = 512); slower below
+    return pz >= 512;
 }
 
 void DemagPlan::release() {

@@ -590,6 +590,168 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     if (pending.kind != U_NONE) sc.signal(pending);
 }
 
+
+// ---------------------------------------------------------------------------
+// warp-FFT variant, L = 512 (n = 256): two lines per warp (fw::fft512x2), so a
+// unit is a pair: A and C take two z rows, B two adjacent ky columns.  The
+// scheduler runs on pair units (n/2 A and C units, L/2 B units per plane);
+// staging layouts are [line][z or y][c], 48 KB per CTA, four CTAs per SM.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(96, 4)
+k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    constexpr int L = 512, N = 256, L2 = L / 2 + 1, NU = N / 2, LU = L / 2;
+    extern __shared__ double2 W[];                 // 3 x 1024
+    __shared__ long long next_ticket;
+    __shared__ int flag;
+    const int hx = a.hx;
+    const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* Wc = W + c * 1024;
+    PipeArgs au = a;
+    au.n = NU;
+    const Sched sc(au, LU, halt);
+    const TicketMap tmap{hx, NU, LU};
+    const double2* __restrict__ Kp2 = reinterpret_cast<const double2*>(a.Kp);
+
+    auto stage = [&](const Unit& u) {
+        double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
+        if (u.kind == U_A) {   // rows 2 idx, 2 idx + 1 of XP: contiguous
+            const double2* src = a.XP + u.plane * plane_xp + (long long)(2 * u.idx) * N * 3;
+            for (int j = threadIdx.x; j < 2 * N * 3; j += 96) cp_async16(&W[j], src + j, true);
+        } else if (u.kind == U_B) {   // columns 2 idx, 2 idx + 1: 96 contiguous bytes per z
+            const int ky0 = 2 * u.idx;
+            for (int j = threadIdx.x; j < 6 * N; j += 96) {
+                const int z = j / 6, r = j - 6 * z, ln = r / 3, cc = r - 3 * ln;
+                cp_async16(&W[(ln * N + z) * 3 + cc], slot + ((long long)z * L + ky0 + ln) * 3 + cc, true);
+            }
+            if (threadIdx.x < 2) {
+                const int ky = ky0 + threadIdx.x, kyq = 2 * ky > L ? L - ky : ky;
+                const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+            }
+        } else {   // slot rows 2 idx, 2 idx + 1: contiguous
+            const double2* src = slot + (long long)(2 * u.idx) * L * 3;
+            for (int j = threadIdx.x; j < 2 * L * 3; j += 96) cp_async16(&W[j], src + j, true);
+        }
+        cp_async_commit();
+    };
+
+    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+    __syncthreads();
+    Unit cur = tmap(next_ticket);
+    Unit pending{U_NONE, 0, 0};
+
+    while (cur.kind != U_NONE) {
+        if (!sc.wait_ready(cur, &flag, pending)) return;
+        stage(cur);
+        cp_async_wait_all();
+        if (pending.kind != U_NONE) {
+            sc.signal(pending);
+            pending.kind = U_NONE;
+        }
+        __syncthreads();
+        double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
+#if MXB_PIPE_DISCARD
+        if (cur.kind == U_C) {
+            char* rows = reinterpret_cast<char*>(slot + (long long)(2 * cur.idx) * L * 3);
+            for (int j = threadIdx.x; j < 2 * L * 3 * 16 / 128; j += 96)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(rows + (size_t)j * 128) : "memory");
+        }
+#endif
+        double2 xa[16], xb[16], v[32];
+        if (cur.kind == U_C) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                xa[m] = W[(lane + 32 * m) * 3 + c];
+                xb[m] = W[(L + lane + 32 * m) * 3 + c];
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                xa[m] = m < 8 ? W[(lane + 32 * m) * 3 + c] : make_double2(0.0, 0.0);
+                xb[m] = m < 8 ? W[(N + lane + 32 * m) * 3 + c] : make_double2(0.0, 0.0);
+            }
+        }
+        __syncthreads();   // W becomes the transpose tiles
+        const int line = lane >> 4, k1 = lane & 15;
+        bool inverse = cur.kind == U_C;
+        if (cur.kind != U_C) {
+            fw::fft512x2<-1>(xa, xb, v, Wc, lane, tw);
+            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            __syncthreads();
+            if (cur.kind == U_A) {
+                // ---- y forward of rows 2 idx (+1) -> slot rows [ky][c]
+#pragma unroll
+                for (int k2 = 0; k2 < 32; ++k2) W[(line * L + k1 + 16 * k2) * 3 + c] = v[fw::p32(k2)];
+                __syncthreads();
+                double2* dst = slot + (long long)(2 * cur.idx) * L * 3;
+                for (int j = threadIdx.x; j < 2 * L * 3; j += 96) st_l2(dst + j, W[j]);
+            } else {
+                // ---- B: * K between the z transforms of columns 2 idx (+1)
+                const int ky0 = 2 * cur.idx;
+#pragma unroll
+                for (int k2 = 0; k2 < 32; ++k2) W[c * 1024 + line * L + k1 + 16 * k2] = v[fw::p32(k2)];
+                __syncthreads();
+                const double s = a.scale;
+                for (int t = threadIdx.x; t < 2 * L; t += 96) {
+                    const int ln = t / L, kz = t - ln * L, ky = ky0 + ln;
+                    const bool fy = 2 * ky > L, fz = 2 * kz > L;
+                    const double2* kr = Kp2 + (((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 +
+                                               (fz ? L - kz : kz)) * 3;
+                    const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
+                    const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                    const double kxy = fy ? -q01.y : q01.y;
+                    const double kxz = fz ? -q23.x : q23.x;
+                    const double kyz = (fy != fz) ? -q45.x : q45.x;
+                    const double2 m0 = W[t], m1 = W[1024 + t], m2 = W[2048 + t];
+                    const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                    kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                    const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                    kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                    const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                    kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                    W[t] = make_double2(h0.x * s, h0.y * s);
+                    W[1024 + t] = make_double2(h1.x * s, h1.y * s);
+                    W[2048 + t] = make_double2(h2.x * s, h2.y * s);
+                }
+                __syncthreads();
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    xa[m] = Wc[lane + 32 * m];
+                    xb[m] = Wc[L + lane + 32 * m];
+                }
+                __syncthreads();   // tiles reused by the inverse
+                inverse = true;
+            }
+        }
+        if (inverse) {
+            fw::fft512x2<1>(xa, xb, v, Wc, lane, tw);
+            if (cur.kind == U_C && threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            __syncthreads();
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) W[(line * N + k1 + 16 * k2) * 3 + c] = v[fw::p32(k2)];   // n < N kept
+            __syncthreads();
+            if (cur.kind == U_C) {
+                // ---- y inverse of rows 2 idx (+1) -> XP rows (contiguous)
+                double2* dst = a.XP + cur.plane * plane_xp + (long long)(2 * cur.idx) * N * 3;
+                for (int j = threadIdx.x; j < 2 * N * 3; j += 96) st_stream(dst + j, W[j]);
+            } else {
+                // ---- B: columns back into the slot (96 contiguous bytes per z)
+                const int ky0 = 2 * cur.idx;
+                for (int j = threadIdx.x; j < 6 * N; j += 96) {
+                    const int z = j / 6, r = j - 6 * z, ln = r / 3, cc = r - 3 * ln;
+                    st_l2(slot + ((long long)z * L + ky0 + ln) * 3 + cc, W[(ln * N + z) * 3 + cc]);
+                }
+            }
+        }
+        __syncthreads();
+        pending = cur;
+        cur = tmap(next_ticket);
+    }
+    if (pending.kind != U_NONE) sc.signal(pending);
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -642,6 +804,39 @@ bool pipe_shape_ok(int ny, int nz) {
     return ny == nz && ny >= 8 && L <= 1024 && (L & (L - 1)) == 0;
 }
 
+static int pipe_launch_warp512(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
+    const size_t smem = (size_t)(3 * 1024) * sizeof(double2);
+    static int grid = 0;
+    if (!grid) {
+        MXB_CUDA(cudaFuncSetAttribute(k_yz_pipe_w512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MXB_CUDA(cudaFuncSetAttribute(k_yz_pipe_w512, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int per_sm = 0;
+        MXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_yz_pipe_w512, 96, smem));
+        if (per_sm < 1) { set_error("pipeline kernel does not fit on an SM"); return MXB_EINVAL; }
+        grid = per_sm * sm_count();
+        if (getenv("MXB_PIPE_VERBOSE")) {
+            cudaFuncAttributes fa;
+            cudaFuncGetAttributes(&fa, k_yz_pipe_w512);
+            fprintf(stderr, "k_yz_pipe_w512: regs %d smem %zu per_sm %d grid %d\n", fa.numRegs, smem, per_sm, grid);
+        }
+    }
+    int g = grid;
+    if (const char* e = getenv("MXB_PIPE_GRID")) g = atoi(e) > 0 ? atoi(e) : g;
+    MXB_CUDA(cudaMemsetAsync(a.sync, 0, (2 + 2 * (size_t)a.hx + 3 * (size_t)a.n) * sizeof(unsigned), st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(96u);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MXB_CUDA(cudaLaunchKernelEx(&cfg, k_yz_pipe_w512, a, tw, halt));
+    return MXB_OK;
+}
+
 static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
     const size_t smem = (size_t)(3 * 1024) * sizeof(double2);
     static int grid = 0;
@@ -684,6 +879,7 @@ int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx,
     const char* we = getenv("MXB_PIPE_WARP");
     const bool warp = !(we && we[0] == '0');
     if (2 * n == 1024 && warp) return pipe_launch_warp(a, tw, st, halt);
+    if (2 * n == 512 && warp) return pipe_launch_warp512(a, tw, st, halt);
     switch (2 * n) {
         case 16: return pipe_launch_L<16>(a, tw, st, halt);
         case 32: return pipe_launch_L<32>(a, tw, st, halt);

@@ -75,3 +75,12 @@ def test_warp_fft_pipeline_matches_five_pass():
         else:
             os.environ["MXB_PIPE_WARP"] = old
     assert np.linalg.norm(hw - h5) <= 1e-13 * np.linalg.norm(h5)
+
+
+@pytest.mark.parametrize("dims", [(64, 256, 256), (8, 256, 256)])
+def test_warp_pair_pipeline_l512_matches_five_pass(dims):
+    """Warp pipeline with two 512-point lines per warp (k_yz_pipe_w512)."""
+    g = mx.GridSpec(*dims, 2e-9, 2.5e-9, 3e-9)
+    m = np.random.default_rng(13).normal(size=(3,) + g.shape) * 8e5
+    hp, h5 = build(g, True).field(m), build(g, False).field(m)
+    assert np.linalg.norm(hp - h5) <= 1e-13 * np.linalg.norm(h5)
