@@ -44,6 +44,9 @@
 #ifndef MXB_PIPE_W_CTAS
 #define MXB_PIPE_W_CTAS 4
 #endif
+#ifndef MXB_PIPE_BULK
+#define MXB_PIPE_BULK 1
+#endif
 #ifndef MXB_PIPE_DISCARD
 #define MXB_PIPE_DISCARD 1
 #endif
@@ -82,6 +85,33 @@ __device__ __forceinline__ void st_l2(double2* p, double2 v) {
 
 __device__ __forceinline__ void st_stream(double2* p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+
+// TMA bulk copy global -> shared completing on an mbarrier (contiguous rows:
+// one instruction instead of one cp.async per 16 bytes per thread)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one thread: expect `bytes` and issue the copy
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mb))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(mb)), "r"(phase)
+            : "memory");
+    }
 }
 
 enum { U_NONE = 0, U_A = 1, U_B = 2, U_C = 3 };
@@ -420,6 +450,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     extern __shared__ double2 sm[];
     __shared__ long long next_ticket;
     __shared__ int flag;
+    __shared__ alignas(8) unsigned long long mbar;           // bulk row copies (A, C)
     double2* W = sm;                                        // 3 x 1024
     // kernel rows are read through the read-only path in the multiply (a
     // warp's 32 consecutive kz rows are 1.5 KB contiguous)
@@ -434,8 +465,13 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     auto stage = [&](const Unit& u) {
         double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
         if (u.kind == U_A) {
+#if MXB_PIPE_BULK
+            if (threadIdx.x == 0)
+                bulk_g2s(W, a.XP + u.plane * plane_xp + (long long)u.idx * N * 3, 3 * N * 16, &mbar);
+#else
             const double2* src = a.XP + u.plane * plane_xp + (long long)u.idx * N * 3;
             for (int j = threadIdx.x; j < 3 * N; j += 96) cp_async16(&W[j], src + j, true);
+#endif
         } else if (u.kind == U_B) {
             const double2* col = slot + (long long)u.idx * 3;
             for (int j = threadIdx.x; j < 3 * N; j += 96) {
@@ -450,10 +486,25 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
             }
         } else {
+#if MXB_PIPE_BULK
+            if (threadIdx.x == 0) bulk_g2s(W, slot + (long long)u.idx * L * 3, 3 * L * 16, &mbar);
+#else
             const double2* src = slot + (long long)u.idx * L * 3;
             for (int j = threadIdx.x; j < 3 * L; j += 96) cp_async16(&W[j], src + j, true);
+#endif
         }
         cp_async_commit();
+    };
+    unsigned mphase = 0;
+    // wait for the staged input of u (cp.async group and, for A and C, the bulk copy)
+    auto stage_wait = [&](const Unit& u) {
+        cp_async_wait_all();
+#if MXB_PIPE_BULK
+        if (u.kind != U_B) {
+            mbar_wait(&mbar, mphase);
+            mphase ^= 1u;
+        }
+#endif
     };
     // registers (lane j holds e = j + 32 k in v[p32(k)], k < NK) -> W natural [e][3]
     // -> contiguous 16-byte stores of the first ne elements (whole sectors per warp)
@@ -469,7 +520,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             for (int j = threadIdx.x; j < 3 * ne; j += 96) st_l2(dst + j, W[j]);
     };
 
-    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+    if (threadIdx.x == 0) {
+        next_ticket = atomicAdd(sc.ticket(), 1u);
+#if MXB_PIPE_BULK
+        mbar_init(&mbar);
+#endif
+    }
     __syncthreads();
     Unit cur = tmap(next_ticket);
     // completion of the previous unit is signalled after this unit's staging
@@ -479,7 +535,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     while (cur.kind != U_NONE) {
         if (!sc.wait_ready(cur, &flag, pending)) return;
         stage(cur);
-        cp_async_wait_all();
+        stage_wait(cur);
         if (pending.kind != U_NONE) {
             sc.signal(pending);
             pending.kind = U_NONE;
