@@ -660,6 +660,7 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
     extern __shared__ double2 W[];                 // 3 x 1024
     __shared__ long long next_ticket;
     __shared__ int flag;
+    __shared__ alignas(8) unsigned long long mbar;  // bulk row copies (A, C)
     const int hx = a.hx;
     const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -673,8 +674,8 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
     auto stage = [&](const Unit& u) {
         double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
         if (u.kind == U_A) {   // rows 2 idx, 2 idx + 1 of XP: contiguous
-            const double2* src = a.XP + u.plane * plane_xp + (long long)(2 * u.idx) * N * 3;
-            for (int j = threadIdx.x; j < 2 * N * 3; j += 96) cp_async16(&W[j], src + j, true);
+            if (threadIdx.x == 0)
+                bulk_g2s(W, a.XP + u.plane * plane_xp + (long long)(2 * u.idx) * N * 3, 2 * N * 3 * 16, &mbar);
         } else if (u.kind == U_B) {   // columns 2 idx, 2 idx + 1: 96 contiguous bytes per z
             const int ky0 = 2 * u.idx;
             for (int j = threadIdx.x; j < 6 * N; j += 96) {
@@ -687,13 +688,16 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
             }
         } else {   // slot rows 2 idx, 2 idx + 1: contiguous
-            const double2* src = slot + (long long)(2 * u.idx) * L * 3;
-            for (int j = threadIdx.x; j < 2 * L * 3; j += 96) cp_async16(&W[j], src + j, true);
+            if (threadIdx.x == 0) bulk_g2s(W, slot + (long long)(2 * u.idx) * L * 3, 2 * L * 3 * 16, &mbar);
         }
         cp_async_commit();
     };
+    unsigned mphase = 0;
 
-    if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+    if (threadIdx.x == 0) {
+        next_ticket = atomicAdd(sc.ticket(), 1u);
+        mbar_init(&mbar);
+    }
     __syncthreads();
     Unit cur = tmap(next_ticket);
     Unit pending{U_NONE, 0, 0};
@@ -702,6 +706,10 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
         if (!sc.wait_ready(cur, &flag, pending)) return;
         stage(cur);
         cp_async_wait_all();
+        if (cur.kind != U_B) {
+            mbar_wait(&mbar, mphase);
+            mphase ^= 1u;
+        }
         if (pending.kind != U_NONE) {
             sc.signal(pending);
             pending.kind = U_NONE;
