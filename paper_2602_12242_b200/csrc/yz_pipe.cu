@@ -37,12 +37,18 @@
 #include <stdlib.h>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "demag.cuh"
 #include "fft_fast.cuh"
 #include "fft_warp.cuh"
 
 #ifndef MXB_PIPE_W_CTAS
 #define MXB_PIPE_W_CTAS 4
+#endif
+#ifndef MXB_PIPE_TMA
+#define MXB_PIPE_TMA 1
 #endif
 #ifndef MXB_PIPE_BULK
 #define MXB_PIPE_BULK 1
@@ -112,6 +118,25 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase
             : "r"(smem_u32(mb)), "r"(phase)
             : "memory");
     }
+}
+
+
+// TMA tensor copies of B's slot columns: the slot array as a 2-D tensor of
+// float64, rows (slot, z) of L * 6 values; a box {6, 256} is 256 z values of
+// one ky column (48 B each) -- [z][c] in shared memory, the staging layout.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* mb) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(mb))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+                 "r"(x), "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
 }
 
 enum { U_NONE = 0, U_A = 1, U_B = 2, U_C = 3 };
@@ -444,10 +469,11 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
 // away.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(96, MXB_PIPE_W_CTAS)
-k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
+k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ halt,
+            const __grid_constant__ CUtensorMap tmap_slot) {
     if (halt && *halt) return;
     constexpr int L = 1024, N = 512, L2 = L / 2 + 1;
-    extern __shared__ double2 sm[];
+    extern __shared__ __align__(128) double2 sm[];
     __shared__ long long next_ticket;
     __shared__ int flag;
     __shared__ alignas(8) unsigned long long mbar;           // bulk row copies (A, C)
@@ -473,11 +499,22 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             for (int j = threadIdx.x; j < 3 * N; j += 96) cp_async16(&W[j], src + j, true);
 #endif
         } else if (u.kind == U_B) {
+#if MXB_PIPE_TMA
+            if (threadIdx.x == 0) {
+                // the column, z 0..255 and 256..511, as two tensor boxes -> W [z][c]
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                mbar_expect(&mbar, 2 * 256 * 48);
+                const int y0 = (u.plane % 3) * N;
+                tma_load_2d(W, &tmap_slot, u.idx * 6, y0, &mbar);
+                tma_load_2d(W + 768, &tmap_slot, u.idx * 6, y0 + 256, &mbar);
+            }
+#else
             const double2* col = slot + (long long)u.idx * 3;
             for (int j = threadIdx.x; j < 3 * N; j += 96) {
                 const int z = j / 3, cc = j - 3 * z;
                 cp_async16(&W[j], col + (long long)z * L * 3 + cc, true);
             }
+#endif
             if (threadIdx.x == 0) {
                 // pull the unit's kernel row (L2 x 48 B) into L2 over the forward FFT;
                 // the multiply reads it through the read-only path
@@ -487,7 +524,10 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             }
         } else {
 #if MXB_PIPE_BULK
-            if (threadIdx.x == 0) bulk_g2s(W, slot + (long long)u.idx * L * 3, 3 * L * 16, &mbar);
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                bulk_g2s(W, slot + (long long)u.idx * L * 3, 3 * L * 16, &mbar);
+            }
 #else
             const double2* src = slot + (long long)u.idx * L * 3;
             for (int j = threadIdx.x; j < 3 * L; j += 96) cp_async16(&W[j], src + j, true);
@@ -500,7 +540,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     auto stage_wait = [&](const Unit& u) {
         cp_async_wait_all();
 #if MXB_PIPE_BULK
-        if (u.kind != U_B) {
+        if (u.kind != U_B || MXB_PIPE_TMA) {
             mbar_wait(&mbar, mphase);
             mphase ^= 1u;
         }
@@ -537,6 +577,11 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         stage(cur);
         stage_wait(cur);
         if (pending.kind != U_NONE) {
+            if (threadIdx.x == 0) {
+                // a B unit's column went out as TMA stores: complete them first
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
             sc.signal(pending);
             pending.kind = U_NONE;
         }
@@ -631,17 +676,34 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 __syncthreads();
 #pragma unroll
                 for (int k = 0; k < 16; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
+#if MXB_PIPE_TMA
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const int y0 = (cur.plane % 3) * N;
+                    tma_store_2d(&tmap_slot, cur.idx * 6, y0, W);
+                    tma_store_2d(&tmap_slot, cur.idx * 6, y0 + 256, W + 768);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    // W is staged into by the next unit: the stores must have read it
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+#else
                 __syncthreads();
                 double2* col = slot + (long long)cur.idx * 3;
                 for (int j = threadIdx.x; j < 3 * N; j += 96) {
                     const int z = j / 3, cc = j - 3 * z;
                     st_l2(col + (long long)z * L * 3 + cc, W[j]);
                 }
+#endif
             }
         }
         __syncthreads();
         pending = cur;
         cur = tmap(next_ticket);
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     if (pending.kind != U_NONE) sc.signal(pending);
 }
@@ -901,6 +963,31 @@ static int pipe_launch_warp512(const PipeArgs& a, const double2* tw, cudaStream_
     return MXB_OK;
 }
 
+// the slot ring as a 2-D float64 tensor: rows (slot, z), L * 6 values each;
+// box {6, 256} = one ky column over 256 z
+static int make_slot_map(CUtensorMap* tm, void* slot, int L, int n) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode) {
+            set_error("cuTensorMapEncodeTiled is not available");
+            return MXB_ECUDA;
+        }
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)L * 6, (cuuint64_t)3 * n};
+    const cuuint64_t strides[1] = {(cuuint64_t)L * 6 * sizeof(double)};
+    const cuuint32_t box[2] = {6, 256}, estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, slot, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed for the slot ring");
+        return MXB_ECUDA;
+    }
+    return MXB_OK;
+}
+
 static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
     const size_t smem = (size_t)(3 * 1024) * sizeof(double2);
     static int grid = 0;
@@ -930,7 +1017,9 @@ static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t s
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MXB_CUDA(cudaLaunchKernelEx(&cfg, k_yz_pipe_w, a, tw, halt));
+    CUtensorMap tm;
+    if (make_slot_map(&tm, a.slot, 1024, a.n)) return MXB_ECUDA;
+    MXB_CUDA(cudaLaunchKernelEx(&cfg, k_yz_pipe_w, a, tw, halt, tm));
     return MXB_OK;
 }
 
