@@ -553,11 +553,26 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         __syncthreads();   // every warp is done with its transpose tile
 #pragma unroll
         for (int k = 0; k < NK; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
+#if MXB_PIPE_TMA
+        // one bulk store of the contiguous row (the next unit stages into W, so
+        // the store must have read it before the end-of-unit barrier)
+        (void)stream;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                         "r"(smem_u32(W)), "r"(3 * ne * 16)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+#else
         __syncthreads();
         if (stream)
             for (int j = threadIdx.x; j < 3 * ne; j += 96) st_stream(dst + j, W[j]);
         else
             for (int j = threadIdx.x; j < 3 * ne; j += 96) st_l2(dst + j, W[j]);
+#endif
     };
 
     if (threadIdx.x == 0) {
