@@ -724,6 +724,204 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 }
 
 
+
+// ---------------------------------------------------------------------------
+// prefetching variant of k_yz_pipe_w (opt-in, MXB_PIPE_PREFETCH=1): three CTAs
+// per SM, each with a 24.6 KB side buffer Q into which the NEXT unit's input is
+// staged by TMA while the current unit computes -- A rows and B columns fit in
+// Q; C rows (49 KB) still stage into W synchronously.  Tickets are fetched two
+// ahead so the next unit is known at the start of the current one.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(96, 3)
+k_yz_pipe_wq(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ halt,
+             const __grid_constant__ CUtensorMap tmap_slot) {
+    if (halt && *halt) return;
+    constexpr int L = 1024, N = 512, L2 = L / 2 + 1;
+    extern __shared__ __align__(128) double2 sm[];
+    __shared__ long long tk_sh;
+    __shared__ int flag, qflag;
+    __shared__ alignas(8) unsigned long long mbar, mbq;
+    double2* W = sm;              // 3 x 1024: staging (C, unprefetched units), tiles, exchange
+    double2* Q = sm + 3 * L;      // 3 x 512: the next A / B unit's input
+    const double2* __restrict__ Kp2 = reinterpret_cast<const double2*>(a.Kp);
+    const int hx = a.hx;
+    const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* Wc = W + c * L;
+    const Sched sc(a, L, halt);
+    const TicketMap tmap{hx, N, L};
+
+    // thread 0: issue the staging of u into dst (A and B only into Q; any into W)
+    auto issue = [&](const Unit& u, double2* dst, unsigned long long* mb) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (u.kind == U_A) {
+            bulk_g2s(dst, a.XP + u.plane * plane_xp + (long long)u.idx * N * 3, 3 * N * 16, mb);
+        } else if (u.kind == U_B) {
+            mbar_expect(mb, 2 * 256 * 48);
+            const int y0 = (u.plane % 3) * N;
+            tma_load_2d(dst, &tmap_slot, u.idx * 6, y0, mb);
+            tma_load_2d(dst + 768, &tmap_slot, u.idx * 6, y0 + 256, mb);
+            const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
+            const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+        } else {
+            const double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
+            bulk_g2s(dst, slot + (long long)u.idx * L * 3, 3 * L * 16, mb);
+        }
+    };
+    auto bulk_store = [&](double2* dst, int nelem) {   // thread 0, after fence + barrier
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(W)),
+                     "r"(nelem * 16)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    };
+
+    Unit pending{U_NONE, 0, 0};
+    long long tk2 = -1;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar);
+        mbar_init(&mbq);
+        flag = (int)atomicAdd(sc.ticket(), 1u);
+        tk_sh = atomicAdd(sc.ticket(), 1u);
+    }
+    __syncthreads();
+    Unit cur = tmap(flag);
+    Unit nxt = tmap(tk_sh);
+    unsigned mph = 0, mpq = 0;
+    bool in_q = false;   // cur's input was prefetched into Q
+
+    while (cur.kind != U_NONE) {
+        if (!in_q) {
+            if (!sc.wait_ready(cur, &flag, pending)) return;
+            if (threadIdx.x == 0) issue(cur, W, &mbar);
+        }
+        bool nxt_ready = false;
+        if (threadIdx.x == 0) {
+            tk2 = atomicAdd(sc.ticket(), 1u);
+            nxt_ready = (nxt.kind == U_A || nxt.kind == U_B) && sc.ready(nxt);
+        }
+        if (in_q) {
+            mbar_wait(&mbq, mpq);
+            mpq ^= 1u;
+        } else {
+            mbar_wait(&mbar, mph);
+            mph ^= 1u;
+        }
+        if (threadIdx.x == 0) {
+            if (pending.kind != U_NONE) {
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                sc.signal(pending);
+                pending.kind = U_NONE;
+            }
+            qflag = nxt_ready;
+        }
+        __syncthreads();
+        const double2* src = in_q ? Q : W;
+        double2 v[32];
+        if (cur.kind == U_C) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = src[(lane + 32 * m) * 3 + c];
+        } else {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = m < 16 ? src[(lane + 32 * m) * 3 + c] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();   // W and Q are free: prefetch the next unit into Q
+        const bool staged_next = qflag != 0;
+        if (staged_next && threadIdx.x == 0) issue(nxt, Q, &mbq);
+        double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
+#if MXB_PIPE_DISCARD
+        if (cur.kind == U_C) {
+            char* row = reinterpret_cast<char*>(slot + (long long)cur.idx * L * 3);
+            for (int j = threadIdx.x; j < 3 * L * 16 / 128; j += 96)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + (size_t)j * 128) : "memory");
+        }
+#endif
+        bool inverse = cur.kind == U_C;
+        if (cur.kind != U_C) {
+            fw::fft1024<-1>(v, Wc, lane, tw);
+            if (cur.kind == U_A) {
+                // ---- y forward of row z = idx -> slot row [ky][c]: one bulk store
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) bulk_store(slot + (long long)cur.idx * L * 3, 3 * L);
+            } else {
+                // ---- B: * K between the z transforms of column ky = idx
+                const int ky = cur.idx;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) Wc[lane + 32 * k] = v[fw::p32(k)];
+                __syncthreads();
+                const bool fy = 2 * ky > L;
+                const double s = a.scale;
+                const double2* krow = Kp2 + ((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 * 3;
+                for (int kz = threadIdx.x; kz < L; kz += 96) {
+                    const bool fz = 2 * kz > L;
+                    const double2* kr = krow + (fz ? L - kz : kz) * 3;
+                    const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
+                    const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                    const double kxy = fy ? -q01.y : q01.y;
+                    const double kxz = fz ? -q23.x : q23.x;
+                    const double kyz = (fy != fz) ? -q45.x : q45.x;
+                    const double2 m0 = W[kz], m1 = W[L + kz], m2 = W[2 * L + kz];
+                    const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                    kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                    const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                    kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                    const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                    kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                    W[kz] = make_double2(h0.x * s, h0.y * s);
+                    W[L + kz] = make_double2(h1.x * s, h1.y * s);
+                    W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
+                }
+                __syncthreads();
+#pragma unroll
+                for (int m = 0; m < 32; ++m) v[m] = Wc[lane + 32 * m];
+                __syncthreads();
+                inverse = true;
+            }
+        }
+        if (inverse) {
+            fw::fft1024<1>(v, Wc, lane, tw);
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) W[(lane + 32 * k) * 3 + c] = v[fw::p32(k)];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (cur.kind == U_C) {
+                    // ---- y inverse of row z = idx -> XP row: one bulk store
+                    bulk_store(a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3, 3 * N);
+                } else {
+                    // ---- B: the column back into the slot as two tensor boxes
+                    const int y0 = (cur.plane % 3) * N;
+                    tma_store_2d(&tmap_slot, cur.idx * 6, y0, W);
+                    tma_store_2d(&tmap_slot, cur.idx * 6, y0 + 256, W + 768);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            tk_sh = tk2;
+            pending = cur;
+        }
+        __syncthreads();
+        cur = nxt;
+        nxt = tmap(tk_sh);
+        in_q = staged_next;
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (pending.kind != U_NONE) sc.signal(pending);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // warp-FFT variant, L = 512 (n = 256): two lines per warp (fw::fft512x2), so a
 // unit is a pair: A and C take two z rows, B two adjacent ky columns.  The
@@ -1003,6 +1201,35 @@ static int make_slot_map(CUtensorMap* tm, void* slot, int L, int n) {
     return MXB_OK;
 }
 
+static int pipe_launch_warpq(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
+    const size_t smem = (size_t)(3 * 1024 + 3 * 512) * sizeof(double2);
+    static int grid = 0;
+    if (!grid) {
+        MXB_CUDA(cudaFuncSetAttribute(k_yz_pipe_wq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MXB_CUDA(cudaFuncSetAttribute(k_yz_pipe_wq, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        int per_sm = 0;
+        MXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_yz_pipe_wq, 96, smem));
+        if (per_sm < 1) { set_error("pipeline kernel does not fit on an SM"); return MXB_EINVAL; }
+        grid = per_sm * sm_count();
+        if (getenv("MXB_PIPE_VERBOSE")) fprintf(stderr, "k_yz_pipe_wq: per_sm %d grid %d\n", per_sm, grid);
+    }
+    MXB_CUDA(cudaMemsetAsync(a.sync, 0, (2 + 2 * (size_t)a.hx + 3 * (size_t)a.n) * sizeof(unsigned), st));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(96u);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUtensorMap tm;
+    if (make_slot_map(&tm, a.slot, 1024, a.n)) return MXB_ECUDA;
+    MXB_CUDA(cudaLaunchKernelEx(&cfg, k_yz_pipe_wq, a, tw, halt, tm));
+    return MXB_OK;
+}
+
 static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
     const size_t smem = (size_t)(3 * 1024) * sizeof(double2);
     static int grid = 0;
@@ -1046,7 +1273,11 @@ int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx,
     // radix-16 pipeline, which is bit-identical to the 5-pass path.
     const char* we = getenv("MXB_PIPE_WARP");
     const bool warp = !(we && we[0] == '0');
-    if (2 * n == 1024 && warp) return pipe_launch_warp(a, tw, st, halt);
+    if (2 * n == 1024 && warp) {
+        const char* pe = getenv("MXB_PIPE_PREFETCH");
+        if (pe && pe[0] == '1') return pipe_launch_warpq(a, tw, st, halt);
+        return pipe_launch_warp(a, tw, st, halt);
+    }
     if (2 * n == 512 && warp) return pipe_launch_warp512(a, tw, st, halt);
     switch (2 * n) {
         case 16: return pipe_launch_L<16>(a, tw, st, halt);
