@@ -16,6 +16,7 @@
 
 #include "demag.cuh"
 #include "fft_warp.cuh"
+#include "tma.cuh"
 
 namespace mxb {
 
@@ -30,9 +31,12 @@ template <bool PM>
 __global__ void __launch_bounds__(96, 4)
 k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __restrict__ out, int CHP,
         long long BLKE, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
-        const int* __restrict__ halt) {
+        const int* __restrict__ halt, const __grid_constant__ CUtensorMap map_main,
+        const __grid_constant__ CUtensorMap map_tail) {
     if (halt && *halt) return;
-    extern __shared__ double2 W[];   // 3 x 1024 transpose tiles, then the [line][kx][c] output pair
+    // 3 x 1024 transpose tiles, then the output pair: [kx][line][c] (plane-major,
+    // TMA boxes of 256 planes x 96 B) or [line][kx][c] (row-major, two bulk rows)
+    extern __shared__ __align__(128) double2 W[];
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * 1024;
     const long long row0 = 2LL * blockIdx.x;
@@ -70,27 +74,30 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
                 xo[ln][i] = cadd(E, cmul(tw1024[kx], Od));
             }
         }
-    __syncthreads();   // every warp is done with its tile: stage [line][kx][c]
+    __syncthreads();   // every warp is done with its tile: stage the output pair
 #pragma unroll
     for (int ln = 0; ln < 2; ++ln)
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
             const int kx = lane + 32 * i;
-            if (kx < XHX) W[(ln * XHX + kx) * 3 + c] = xo[ln][i];
+            if (kx < XHX) W[PM ? (kx * 2 + ln) * 3 + c : (ln * XHX + kx) * 3 + c] = xo[ln][i];
         }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (PM) {
-        // out[kx][row][c]: the pair's 6 values per bin are contiguous
-        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
-            const int kx = j / 6, r = j - 6 * kx, ln = r / 3, cc = r - 3 * ln;
-            out[(long long)kx * BLKE + (row0 + ln) * 3 + cc] = W[(ln * XHX + kx) * 3 + cc];
+    if (threadIdx.x == 0) {
+        if (PM) {
+            // out[kx][row][c]: the pair's 96 bytes per plane, as TMA boxes of 256 planes
+            const int x = (int)(row0 * 6);
+            tma_store_2d(&map_main, x, 0, W);
+            tma_store_2d(&map_main, x, 256, W + 256 * 6);
+            tma_store_2d(&map_tail, x, 512, W + 512 * 6);
+        } else {
+            // out[row][kx][c]: two contiguous rows of XHX * 48 bytes
+            bulk_s2g(out + (row0 * CHP) * 3, W, XHX * 48);
+            bulk_s2g(out + ((row0 + 1) * CHP) * 3, W + XHX * 3, XHX * 48);
         }
-    } else {
-        // out[row][kx][c]: XHX * 3 contiguous values per row
-        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
-            const int ln = j / (XHX * 3), r = j - ln * XHX * 3;
-            out[((row0 + ln) * CHP) * 3 + r] = W[ln * XHX * 3 + r];
-        }
+        bulk_commit();
+        bulk_wait_all();   // complete before the CTA exits (smem is released)
     }
 }
 
@@ -98,25 +105,31 @@ template <bool PM>
 __global__ void __launch_bounds__(96, 4)
 k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restrict__ out, long long cstride,
         int pitch, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
-        const int* __restrict__ halt) {
+        const int* __restrict__ halt, const __grid_constant__ CUtensorMap map_main,
+        const __grid_constant__ CUtensorMap map_tail) {
     if (halt && *halt) return;
-    extern __shared__ double2 S[];                 // [line][kx][c] input pair, then 3 x 1024 tiles
+    // the input pair ([kx][line][c] by TMA boxes, or [line][kx][c] by two bulk
+    // rows), then 3 x 1024 transpose tiles
+    extern __shared__ __align__(128) double2 S[];
+    __shared__ alignas(8) unsigned long long mbar;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long row0 = 2LL * blockIdx.x;
-    if (PM) {
-        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
-            const int kx = j / 6, r = j - 6 * kx, ln = r / 3, cc = r - 3 * ln;
-            cp_async16(&S[(ln * XHX + kx) * 3 + cc], X + (long long)kx * BLKE + (row0 + ln) * 3 + cc, true);
-        }
-    } else {
-        for (int j = threadIdx.x; j < XHX * 6; j += 96) {
-            const int ln = j / (XHX * 3), r = j - ln * XHX * 3;
-            cp_async16(&S[ln * XHX * 3 + r], X + (row0 + ln) * CHP * 3 + r, true);
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar);
+        if (PM) {
+            mbar_expect(&mbar, XHX * 96);
+            const int x = (int)(row0 * 6);
+            tma_load_2d(S, &map_main, x, 0, &mbar);
+            tma_load_2d(S + 256 * 6, &map_main, x, 256, &mbar);
+            tma_load_2d(S + 512 * 6, &map_tail, x, 512, &mbar);
+        } else {
+            mbar_expect(&mbar, 2 * XHX * 48);
+            bulk_g2s_tx(S, X + row0 * CHP * 3, XHX * 48, &mbar);
+            bulk_g2s_tx(S + XHX * 3, X + (row0 + 1) * CHP * 3, XHX * 48, &mbar);
         }
     }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();   // mbarrier initialised before anyone polls it
+    mbar_wait(&mbar, 0);
     double2 a[16], b[16], v[32];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -124,8 +137,8 @@ k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restri
         const double2 w = tw1024[k];
 #pragma unroll
         for (int ln = 0; ln < 2; ++ln) {
-            const double2 xk = S[(ln * XHX + k) * 3 + c];
-            const double2 xm = S[(ln * XHX + (XM - k)) * 3 + c];
+            const double2 xk = S[PM ? (k * 2 + ln) * 3 + c : (ln * XHX + k) * 3 + c];
+            const double2 xm = S[PM ? ((XM - k) * 2 + ln) * 3 + c : (ln * XHX + (XM - k)) * 3 + c];
             // Z = (Xk + conj Xm) + i (Xk - conj Xm) W^-k
             const double2 A = make_double2(xk.x + xm.x, xk.y - xm.y);
             const double2 Bm = make_double2(xk.x - xm.x, xk.y + xm.y);
@@ -165,12 +178,20 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
             MXB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attrs = true;
     }
+    // plane-major spectra as a 2-D float64 tensor: one row of nrows * 6 values
+    // per kx plane; boxes of {2 rows x 3 components x 2, 256 | 1 planes}
+    CUtensorMap mm{}, mt{};
+    if (pm) {
+        const unsigned long long inner = (unsigned long long)nrows * 6, pitch_b = (unsigned long long)BLKE * 16;
+        if (make_map_2d_f64(&mm, X, inner, XHX, pitch_b, 12, 256) || make_map_2d_f64(&mt, X, inner, XHX, pitch_b, 12, 1))
+            return MXB_ECUDA;
+    }
     if (fwd) {
-        if (pm) k_r2c_w<true><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt);
-        else k_r2c_w<false><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt);
+        if (pm) k_r2c_w<true><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt);
+        else k_r2c_w<false><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt);
     } else {
-        if (pm) k_c2r_w<true><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt);
-        else k_c2r_w<false><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt);
+        if (pm) k_c2r_w<true><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt);
+        else k_c2r_w<false><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;

@@ -37,10 +37,8 @@
 #include <stdlib.h>
 #include <type_traits>
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "demag.cuh"
+#include "tma.cuh"
 #include "fft_fast.cuh"
 #include "fft_warp.cuh"
 
@@ -93,51 +91,6 @@ __device__ __forceinline__ void st_stream(double2* p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-
-// TMA bulk copy global -> shared completing on an mbarrier (contiguous rows:
-// one instruction instead of one cp.async per 16 bytes per thread)
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* mb) {
-    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// one thread: expect `bytes` and issue the copy
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(mb))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned phase) {
-    unsigned done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(mb)), "r"(phase)
-            : "memory");
-    }
-}
-
-
-// TMA tensor copies of B's slot columns: the slot array as a 2-D tensor of
-// float64, rows (slot, z) of L * 6 values; a box {6, 256} is 256 z values of
-// one ky column (48 B each) -- [z][c] in shared memory, the staging layout.
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* mb) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(mb))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
-                 "r"(x), "r"(y), "r"(smem_u32(src))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long* mb, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
-}
 
 enum { U_NONE = 0, U_A = 1, U_B = 2, U_C = 3 };
 
@@ -1179,26 +1132,8 @@ static int pipe_launch_warp512(const PipeArgs& a, const double2* tw, cudaStream_
 // the slot ring as a 2-D float64 tensor: rows (slot, z), L * 6 values each;
 // box {6, 256} = one ky column over 256 z
 static int make_slot_map(CUtensorMap* tm, void* slot, int L, int n) {
-    static PFN_cuTensorMapEncodeTiled encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !encode) {
-            set_error("cuTensorMapEncodeTiled is not available");
-            return MXB_ECUDA;
-        }
-    }
-    const cuuint64_t dims[2] = {(cuuint64_t)L * 6, (cuuint64_t)3 * n};
-    const cuuint64_t strides[1] = {(cuuint64_t)L * 6 * sizeof(double)};
-    const cuuint32_t box[2] = {6, 256}, estr[2] = {1, 1};
-    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, slot, dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed for the slot ring");
-        return MXB_ECUDA;
-    }
-    return MXB_OK;
+    return make_map_2d_f64(tm, slot, (unsigned long long)L * 6, 3ULL * n, (unsigned long long)L * 6 * sizeof(double),
+                           6, 256);
 }
 
 static int pipe_launch_warpq(const PipeArgs& a, const double2* tw, cudaStream_t st, const int* halt) {
