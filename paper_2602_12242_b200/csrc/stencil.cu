@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "stencil.cuh"
+#include "tma.cuh"
 
 namespace mxb {
 
@@ -501,7 +502,8 @@ __device__ void reduce_partials(const double* partials, int nblk, const bool is_
 template <int MODE, bool E>
 __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, const CellMat& cm,
                                            const double m[3], const double h[3], double red[4],
-                                           const double* y_pre = nullptr) {
+                                           const double* y_pre = nullptr, const double* k1_pre = nullptr,
+                                           const double* s_pre = nullptr) {
     const long long N = a.g.N;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
         if (MODE == M_HEFF) {
@@ -524,12 +526,13 @@ __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, co
                     a.s[idx] = kk[0]; a.s[N + idx] = kk[1]; a.s[2 * N + idx] = kk[2];
                 } else if (MODE == M_RK3) {
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(a.s[q * N + idx], kk[q]);
+                    for (int q = 0; q < 3; ++q) a.s[q * N + idx] = add<E>(s_pre ? s_pre[q] : a.s[q * N + idx], kk[q]);
                 }
             } else {  // M_RK4
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    const double k1 = ld(a.k1, q * N + idx), s = a.s[q * N + idx];
+                    const double k1 = k1_pre ? k1_pre[q] : ld(a.k1, q * N + idx);
+                    const double s = s_pre ? s_pre[q] : a.s[q * N + idx];
                     v[q] = add<E>(y[q], mul<E>(a.dt6, add<E>(add<E>(k1, mul<E>(2.0, s)), kk[q])));
                 }
             }
@@ -827,6 +830,148 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZM_CTAS) k_stage_zm(StageArgs a
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA variant of the z-marching stage kernel (single rank, even nx): the state
+// planes (tile + one-cell halo ring, 3 components) arrive as 4-D tensor boxes
+// {34, 10, 1, 3} in a four-plane ring, plane k+2 issued at the start of plane
+// k; the per-plane inputs the mode reads (demag field, step-start state, K1,
+// S) as boxes {32, 8, 1, 3} in a two-plane ring.  All loads complete on
+// mbarriers, so nothing is prefetched into registers and the arithmetic is
+// that of k_stage_zm (bit-identical results).
+// ---------------------------------------------------------------------------
+struct ZtMaps {
+    CUtensorMap st;                 // ys with halo boxes
+    CUtensorMap aux[4];             // hd, y, k1, s (as needed)
+};
+
+template <int MODE> struct ZtAux {
+    static constexpr bool kY = MODE >= M_RK1, kK1 = MODE == M_RK4, kS = MODE == M_RK3 || MODE == M_RK4;
+};
+
+template <int MODE, bool E>
+__global__ void __launch_bounds__(ZTX * ZTY, 2) k_stage_zt(StageArgs a, const __grid_constant__ ZtMaps maps,
+                                                            int nfields, int has_hd) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
+    // state box (doubles): the x origin of a TMA box must be 16-byte aligned,
+    // so the box starts two cells left of the tile (i0 - 2) and one row above
+    constexpr int SX = ZTX + 4, SY = ZTY + 2, SBOX = 3 * SY * SX;
+    constexpr int SPL = (SBOX + 15) / 16 * 16;                          // slot stride: 128-byte aligned
+    constexpr int APL = 3 * ZTY * ZTX;                              // one aux field plane
+    extern __shared__ __align__(128) double zsm[];
+    double* stp = zsm;                       // [4][3][SY][SX]
+    double* aux = zsm + 4 * SPL;             // [2][nfields][3][ZTY][ZTX]
+    __shared__ alignas(8) unsigned long long mst[4], max_[2];
+    const Grid& g = a.g;
+    const long long plane = (long long)g.nx * g.ny;
+    const int tx = threadIdx.x & (ZTX - 1), ty = threadIdx.x / ZTX;
+    const int i0 = blockIdx.x * ZTX, j0 = blockIdx.y * ZTY;
+    const int i = i0 + tx, j = j0 + ty;
+    const int k0 = blockIdx.z * ZC, k1 = min(k0 + ZC, g.nz);
+    const bool in = i < g.nx && j < g.ny;
+    const long long col = (long long)j * g.nx + i;
+    const CellMat cm = cell_mat<E, true>(a, 0);
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    const unsigned st_bytes = SBOX * 8, aux_bytes = nfields * APL * 8;
+
+    auto issue_state = [&](int kk) {   // thread 0
+        unsigned long long* mb = &mst[(kk + 4) & 3];
+        mbar_expect(mb, st_bytes);
+        tma_load_4d(stp + ((kk + 4) & 3) * SPL, &maps.st, i0 - 2, j0 - 1, kk, 0, mb);
+    };
+    auto issue_aux = [&](int kk) {     // thread 0
+        unsigned long long* mb = &max_[kk & 1];
+        mbar_expect(mb, aux_bytes);
+        for (int f = 0; f < nfields; ++f)
+            tma_load_4d(aux + ((kk & 1) * nfields + f) * APL, &maps.aux[f], i0, j0, kk, 0, mb);
+    };
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) mbar_init(&mst[q]);
+        mbar_init(&max_[0]);
+        mbar_init(&max_[1]);
+        issue_state(k0 - 1);
+        issue_state(k0);
+        issue_state(k0 + 1);
+        if (nfields) issue_aux(k0);
+    }
+    __syncthreads();
+    unsigned sph = 0, aph = 0;   // phase bit per slot
+    auto wait_state = [&](int kk) {
+        const int sl = (kk + 4) & 3;
+        mbar_wait(&mst[sl], (sph >> sl) & 1u);
+        sph ^= 1u << sl;
+    };
+    wait_state(k0 - 1);
+    wait_state(k0);
+    for (int k = k0; k < k1; ++k) {
+        if (threadIdx.x == 0) {
+            if (k + 2 <= k1) issue_state(k + 2);          // slot of plane k - 2
+            if (nfields && k + 1 < k1) issue_aux(k + 1);  // slot of plane k - 1
+        }
+        wait_state(k + 1);
+        if (nfields) {
+            mbar_wait(&max_[k & 1], (aph >> (k & 1)) & 1u);
+            aph ^= 1u << (k & 1);
+        }
+        if (in) {
+            const double* sc = stp + ((k + 4) & 3) * SPL;
+            const double* sp = stp + ((k + 5) & 3) * SPL;
+            const double* sm1 = stp + ((k + 3) & 3) * SPL;
+            auto S = [&](const double* b, int q, int yy, int xx) { return b[(q * SY + yy) * SX + xx]; };
+            const long long idx = (long long)k * plane + col;
+            double m[3], xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                m[q] = S(sc, q, ty + 1, tx + 2);
+                xp[q] = S(sc, q, ty + 1, tx + 3);
+                xm[q] = S(sc, q, ty + 1, tx + 1);
+                yp[q] = S(sc, q, ty + 2, tx + 2);
+                ym[q] = S(sc, q, ty, tx + 2);
+                zp[q] = S(sp, q, ty + 1, tx + 2);
+                zm[q] = S(sm1, q, ty + 1, tx + 2);
+            }
+            const bool zp_ok = k + 1 < g.nz, zm_ok = k > 0;
+            const double hf = a.dv.face, A = cm.A, p = cm.slope_p;
+            const bool okxp = i + 1 < g.nx, okxm = i > 0, okyp = j + 1 < g.ny, okym = j > 0;
+            if (!okxp) ghost_nb<E>(a, 0, +1, m, p, xp);
+            if (!okxm) ghost_nb<E>(a, 0, -1, m, p, xm);
+            if (!okyp) ghost_nb<E>(a, 1, +1, m, p, yp);
+            if (!okym) ghost_nb<E>(a, 1, -1, m, p, ym);
+            if (!zp_ok) ghost_nb<E>(a, 2, +1, m, p, zp);
+            if (!zm_ok) ghost_nb<E>(a, 2, -1, m, p, zm);
+            // aux fields in the order hd (if any), y, k1, s
+            const double* ab = aux + (k & 1) * nfields * APL;
+            double hdv[3], yv[3], k1v[3], sv[3];
+            int f = 0;
+            auto A3 = [&](int ff, double v[3]) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) v[q] = ab[ff * APL + (q * ZTY + ty) * ZTX + tx];
+            };
+            if (has_hd) A3(f++, hdv);
+            if (ZtAux<MODE>::kY) A3(f++, yv);
+            if (ZtAux<MODE>::kK1) A3(f++, k1v);
+            if (ZtAux<MODE>::kS) A3(f++, sv);
+            double h[3];
+            heff_nb<E, true>(a, a.ys, idx, i, j, k, m, cm, a.terms, xp, xm, yp, ym, zp, zm,
+                             okxp ? hf : A, okxm ? hf : A, okyp ? hf : A, okym ? hf : A,
+                             zp_ok ? hf : A, zm_ok ? hf : A, h, has_hd ? hdv : nullptr);
+            stage_tail<MODE, E>(a, idx, cm, m, h, red, ZtAux<MODE>::kY ? yv : nullptr,
+                                ZtAux<MODE>::kK1 ? k1v : nullptr, ZtAux<MODE>::kS ? sv : nullptr);
+        }
+        __syncthreads();   // slots of planes k - 1 (state) and k (aux) are reused next
+    }
+    if (kFinal) {
+        const bool is_max[4] = {false, false, false, true};
+        block_reduce<4>(red, is_max);
+        if (threadIdx.x == 0) {
+            const long long b = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            double* pp = a.partials + b * kReduceSlots;
+            pp[0] = red[0]; pp[1] = red[1]; pp[2] = red[2]; pp[3] = red[3];
+        }
+    }
+}
+
 static dim3 zm_grid(const Grid& g) {
     return dim3((g.nx + ZTX - 1) / ZTX, (g.ny + ZTY - 1) / ZTY, (g.nz + ZC - 1) / ZC);
 }
@@ -850,10 +995,55 @@ int stage_nparts(const StageArgs& a) {
     return stage_blocks(a.g.N);
 }
 
+// 4-D float64 map of a (3, nz, ny, nx) field, box {bx, by, 1, 3}
+static int field_map(CUtensorMap* tm, const double* f, const Grid& g, unsigned bx, unsigned by) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode)
+            return MXB_ECUDA;
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz, 3};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.nx * 8, (cuuint64_t)g.nx * g.ny * 8, (cuuint64_t)g.N * 8};
+    const cuuint32_t box[4] = {bx, by, 1, 3}, estr[4] = {1, 1, 1, 1};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(f), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+               ? MXB_OK
+               : MXB_ECUDA;
+}
+
+template <int MODE, bool E>
+static bool launch_zt(const StageArgs& a, cudaStream_t st) {
+    const char* ze = getenv("MXB_ZTMA");   // read per launch: tests switch it
+    const bool on = !(ze && ze[0] == '0');
+    if (!on || a.halo_lo || a.halo_hi || (a.g.nx & 1)) return false;
+    ZtMaps mp;
+    if (field_map(&mp.st, a.ys, a.g, ZTX + 4, ZTY + 2)) return false;
+    int nf = 0;
+    const int has_hd = (a.terms & MXB_TERM_DEMAG) && a.hd ? 1 : 0;
+    if (has_hd && field_map(&mp.aux[nf++], a.hd, a.g, ZTX, ZTY)) return false;
+    if (ZtAux<MODE>::kY && field_map(&mp.aux[nf++], a.y, a.g, ZTX, ZTY)) return false;
+    if (ZtAux<MODE>::kK1 && field_map(&mp.aux[nf++], a.k1, a.g, ZTX, ZTY)) return false;
+    if (ZtAux<MODE>::kS && field_map(&mp.aux[nf++], a.s, a.g, ZTX, ZTY)) return false;
+    const size_t smem = (size_t)(4 * ((3 * (ZTY + 2) * (ZTX + 4) + 15) / 16 * 16) + 2 * nf * 3 * ZTY * ZTX) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_stage_zt<MODE, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+    }
+    k_stage_zt<MODE, E><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd);
+    return true;
+}
+
 template <int MODE>
 static void launch_zm(bool exact, const StageArgs& a, cudaStream_t st) {
-    if (exact) k_stage_zm<MODE, true><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
-    else k_stage_zm<MODE, false><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
+    if (exact) {
+        if (!launch_zt<MODE, true>(a, st)) k_stage_zm<MODE, true><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
+    } else {
+        if (!launch_zt<MODE, false>(a, st)) k_stage_zm<MODE, false><<<zm_grid(a.g), ZTX * ZTY, 0, st>>>(a);
+    }
 }
 
 template <int MODE, bool E>
