@@ -13,6 +13,10 @@
 // constant zero / never stored).
 #pragma once
 
+#ifndef MXB_HALF_IN
+#define MXB_HALF_IN 1   // zero-padded forward inputs skip the zero half of the first stage
+#endif
+
 #include "fft_fast.cuh"
 #include "fft_generic.cuh"
 
@@ -79,6 +83,23 @@ template <int DIR> __device__ __forceinline__ void dft32(double2 (&v)[32]) {
     for (int k1 = 0; k1 < 4; ++k1) dft8<DIR>(&v[8 * k1]);
 }
 
+// dft32 for inputs v[16..31] == 0 (a zero-padded line): the first radix-4
+// stage reduces to {a + b, a - i b, a - b, a + i b} (DIR = -1 sign shown), and
+// the zero registers are never read.  Equal to dft32 up to the sign of zeros
+// (x + 0 is not foldable to x under IEEE rules, so the compiler keeps them).
+template <int DIR> __device__ __forceinline__ void dft32_half(double2 (&v)[32]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) {
+        const double2 a = v[n2], b = v[8 + n2];
+        const double2 ib = mul_mi<DIR>(b);
+        const double2 q[4] = {cadd(a, b), cadd(a, ib), csub(a, b), csub(a, ib)};
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[8 * k1 + n2] = w32<DIR>(q[k1], n2 * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft8<DIR>(&v[8 * k1]);
+}
+
 __host__ __device__ constexpr int p32(int k) { return 8 * (k % 4) + k / 4; }
 
 // transpose tile: row r (the step-1 frequency), column l (the lane)
@@ -86,14 +107,16 @@ __device__ __forceinline__ int tsw(int r, int l) { return r * 32 + (l ^ (r & 7))
 
 // v[m] = x[lane + 32 m] on entry; lane j holds X[j + 32 k] in v[p32(k)] on exit.
 // W: this warp's 1024-element tile (free on entry, clobbered).
-template <int DIR>
+// HALF_IN: x[n] == 0 for n >= 512 (v[16..31] are not read).
+template <int DIR, bool HALF_IN = false>
 __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_in, const double2* __restrict__ tw) {
     // an opaque copy of the lane index: the lane-dependent tile addresses are
     // then recomputed per call instead of being hoisted out of the caller's
     // loop (32 live addresses that end up spilled)
     int lane = lane_in;
     asm volatile("" : "+r"(lane));
-    dft32<DIR>(v);
+    if (HALF_IN) dft32_half<DIR>(v);
+    else dft32<DIR>(v);
     __syncwarp();
     // w1024^(lane k) as a running product, re-anchored from the exact table
     // every 8 steps (<= 7 products; loading all 31 would pin ~120 registers)
@@ -117,18 +140,44 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_i
 }
 
 
+// DFT-16 (as ff::DFT<16>) for inputs x[8..15] == 0
+template <int DIR> __device__ __forceinline__ void dft16_half(double2 (&x)[16]) {
+    double2 y[16];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const double2 a = x[b], c = x[4 + b];
+        const double2 ic = mul_mi<DIR>(c);
+        const double2 q[4] = {cadd(a, c), cadd(a, ic), csub(a, c), csub(a, ic)};
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) y[4 * b + k1] = ff::wmul<DIR>(q[k1], b * k1);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        double2 q[4] = {y[k1], y[4 + k1], y[8 + k1], y[12 + k1]};
+        dft4<DIR>(q);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = q[k2];
+    }
+}
+
 // Two lines of length 512 = 32 x 16 per warp (the x passes: one line per row
 // and component).  Lane l holds xa[l + 32 m] in a[m] and xb[l + 32 m] in b[m]
 // (m < 16).  DFT-16 over m in registers, w512^(l k1) twiddles, one transpose
 // whose 32 tile rows are (line, k1), DFT-32 over l.  On exit lane j holds
 // X_line[k1 + 16 k2] in v[p32(k2)] with line = j >> 4, k1 = j & 15.
-template <int DIR>
+// HALF_IN: a[8..15] and b[8..15] are zero (not read).
+template <int DIR, bool HALF_IN = false>
 __device__ __forceinline__ void fft512x2(double2 (&a)[16], double2 (&b)[16], double2 (&v)[32], double2* W,
                                          int lane_in, const double2* __restrict__ tw512) {
     int lane = lane_in;
     asm volatile("" : "+r"(lane));
-    ff::DFT<16, DIR>::run(a);
-    ff::DFT<16, DIR>::run(b);
+    if (HALF_IN) {
+        dft16_half<DIR>(a);
+        dft16_half<DIR>(b);
+    } else {
+        ff::DFT<16, DIR>::run(a);
+        ff::DFT<16, DIR>::run(b);
+    }
     __syncwarp();
     const double2 w1 = twid<DIR>(tw512, lane);
     double2 w = make_double2(1.0, 0.0);

@@ -578,7 +578,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         __syncthreads();   // W becomes the transpose tiles
         bool inverse = cur.kind == U_C;
         if (cur.kind != U_C) {
-            fw::fft1024<-1>(v, Wc, lane, tw);
+            fw::fft1024<-1, MXB_HALF_IN != 0>(v, Wc, lane, tw);
             if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
             if (cur.kind == U_A) {
                 // ---- y forward of row z = idx -> slot row [ky][c]
@@ -793,7 +793,7 @@ k_yz_pipe_wq(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__
 #endif
         bool inverse = cur.kind == U_C;
         if (cur.kind != U_C) {
-            fw::fft1024<-1>(v, Wc, lane, tw);
+            fw::fft1024<-1, MXB_HALF_IN != 0>(v, Wc, lane, tw);
             if (cur.kind == U_A) {
                 // ---- y forward of row z = idx -> slot row [ky][c]: one bulk store
                 __syncthreads();

@@ -38,3 +38,17 @@ for chunk in (1, 10):
     sim.run_until(mx.StopCondition(max_steps=10))
     el = time.perf_counter() - t0
     print(f"run_until 10 steps CHUNK={chunk}: {1e3*el:.0f} ms -> {N*10/el:.3e} cell-steps/s", flush=True)
+if "--profile" in sys.argv:
+    import cProfile
+    import pstats
+    st = mx.SimState(mx.VectorField3(g, host))
+    sim = mx.Simulation(st, rhs, mx.IntegratorSpec("rk4", dt), sample_every=1, energy_in_samples=False)
+    sim.CHUNK = 1
+    pr = cProfile.Profile()
+    t0 = time.perf_counter()
+    pr.enable()
+    sim.run_until(mx.StopCondition(max_steps=20))
+    pr.disable()
+    el = time.perf_counter() - t0
+    print(f"profiled run_until 20 steps: {1e3*el:.0f} ms -> {N*20/el:.3e}", flush=True)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(14)
