@@ -262,7 +262,7 @@ def main():
         out = {"metric": METRIC, "value": cs, "unit": "cell-steps/s", "n_gpus": args.gpus,
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": 1e3 * el / max(args.steps, 1), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "impl": "reference",
                "config": {"workload": f"synthetic random-m {args.cpu_n}^3 full H_eff RK4 "
                                       f"(bounded CPU sample of the {args.size}^3 workload)"},
@@ -374,7 +374,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"synthetic random-m {args.size}^3, full H_eff "
                                "(demag+exchange+DMI+uniaxial anis+Zeeman), RK4",
