@@ -22,6 +22,10 @@ namespace mxb {
 
 using namespace ff;
 
+#ifndef MXB_XW_TMA_IN
+#define MXB_XW_TMA_IN 1   // r2c input rows staged by TMA bulk copies
+#endif
+
 namespace {
 constexpr int XM = 512;          // complex FFT length (px / 2)
 constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
@@ -40,14 +44,37 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * 1024;
     const long long row0 = 2LL * blockIdx.x;
+    double2 a[16], b[16], v[32];
+#if MXB_XW_TMA_IN
+    // the row pair of each component is 8 KB contiguous (pitch == nx): three
+    // bulk copies into the (still free) tile memory, one mbarrier wait
+    __shared__ alignas(8) unsigned long long mbar;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar);
+        mbar_expect(&mbar, 3 * 2 * XM * 8);
+        for (int q = 0; q < 3; ++q)
+            bulk_g2s_tx(W + q * XM, in + q * cstride + row0 * pitch, 2 * XM * 8, &mbar);
+    }
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    {
+        const double2* s0 = W + c * XM;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {   // packed pairs (x[2n], x[2n+1]), n < 256 non-zero
+            a[m] = m < 8 ? s0[lane + 32 * m] : make_double2(0.0, 0.0);
+            b[m] = m < 8 ? s0[XM / 2 + lane + 32 * m] : make_double2(0.0, 0.0);
+        }
+    }
+    __syncthreads();   // the staged rows are in registers: the tiles may overwrite them
+#else
     const double2* s0 = reinterpret_cast<const double2*>(in + c * cstride + row0 * pitch);
     const double2* s1 = reinterpret_cast<const double2*>(in + c * cstride + (row0 + 1) * pitch);
-    double2 a[16], b[16], v[32];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {   // packed pairs (x[2n], x[2n+1]), n < 256 non-zero
         a[m] = m < 8 ? __ldg(s0 + lane + 32 * m) : make_double2(0.0, 0.0);
         b[m] = m < 8 ? __ldg(s1 + lane + 32 * m) : make_double2(0.0, 0.0);
     }
+#endif
     fw::fft512x2<-1>(a, b, v, Wc, lane, tw512);   // HALF_IN measured 1% slower here
     // Z_line[k1 + 16 k2] -> tile, natural order per line
     {
