@@ -134,6 +134,22 @@ def demag_bytes(g, kern, survey=True):
     return [24 * N + x1, x1 + x2, 2 * x2 + kbytes, x2 + x1, x1 + 24 * N]
 
 
+def demag_flops(g, kern):
+    """FP64 flops of one demag evaluation per pass: 2.5 L log2 L per
+    real line transform, 5 L log2 L per complex line, over the pruned lines,
+    plus 36 per spectral point for the 3x3 multiply."""
+    import math
+    nx, ny, nz = g.nx, g.ny, g.nz
+    pz, py, px = kern.padded
+    hx = px // 2 + 1
+    lg = lambda n: math.log2(n) if n > 1 else 0.0
+    xr = 3 * ny * nz * 2.5 * px * lg(px)
+    yc = 3 * hx * nz * 5 * py * lg(py)
+    zc = 3 * hx * py * 5 * pz * lg(pz)
+    mul = 36 * hx * py * pz
+    return [xr, yc, 2 * zc + mul, yc, xr]
+
+
 def cpu_reference(n: int, steps: int, warmup: int):
     """Oracle (numpy/scipy restatement of the reference) RK4 on a bounded
     sample of the same workload: an n^3 grid, all host threads for the FFTs."""
@@ -341,6 +357,19 @@ def main():
             traffic = json.load(f).get(dom[0])
     except Exception:
         pass
+    pf = demag_flops(g, kern)
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            fpk = float(json.load(f)["fp64_tflops"])
+        t_yz = (passes[1] + passes[2] + passes[3]) * 1e-3
+        fp64 = {"gflop_per_eval": sum(pf) / 1e9, "eval_tflops": sum(pf) / (ms_eval.value * 1e-3) / 1e12,
+                "yz_tflops": (pf[1] + pf[2] + pf[3]) / t_yz / 1e12, "peak_tflops": fpk,
+                "yz_frac": (pf[1] + pf[2] + pf[3]) / t_yz / 1e12 / fpk,
+                "peak_source": "profiles/fp64_peak.json (tools/micro/fp64_peak.cu, DFMA chains)",
+                "flops": "SURVEY 8d formula"}
+    except Exception:
+        pass
     step_bytes = stencil_bytes + 4 * sum(pb)
     step_bytes_own = stencil_bytes + 4 * sum(pb_own)
     # end to end through the public API with host buffers
@@ -392,6 +421,7 @@ def main():
         "kernels_ms_per_step": share,
         "timing": {"repeats": len(runs), "ms_per_step_runs": runs, "statistic": "median",
                    "clock": "CUDA events on the solver stream"},
+        "fp64": fp64,
         "demag_ms_per_eval": ms_eval.value, "cufft_demag_ms_per_eval": ms_cufft.value,
         "tensor_build_s": t_build,
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(nl.value),
