@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmagnex_b200.so")
-SOURCES = ["api.cu", "stencil.cu", "demag.cu", "demag_fast.cu", "newell.cu", "yz_pipe.cu", "x_warp.cu", "fno.cu", "cufft_compare.cu"]
+SOURCES = ["api.cu", "stencil.cu", "demag.cu", "demag_fast.cu", "newell.cu", "yz_pipe.cu", "x_warp.cu", "longy.cu", "fno.cu", "cufft_compare.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

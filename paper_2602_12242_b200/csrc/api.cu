@@ -392,10 +392,10 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
                     }
         return MXB_OK;
     }
-    if (p.kmode == 3) {
+    if (p.kmode == 3 || p.kmode == 4) {
         // plane-major quarter storage Kp[kx][ky'][kz'][6]
-        const int L2 = p.pz / 2 + 1;
-        const size_t n = (size_t)p.hx * L2 * L2 * 6;
+        const int Y2 = p.py / 2 + 1, Z2 = p.pz / 2 + 1;
+        const size_t n = (size_t)p.hx * Y2 * Z2 * 6;
         std::vector<double> h(n);
         MXB_CUDA(cudaMemcpy(h.data(), p.Kp, n * sizeof(double), cudaMemcpyDeviceToHost));
         for (int c = 0; c < 6; ++c)
@@ -408,7 +408,7 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
                     if (c == 2 && fz) sgn = -1.0;
                     if (c == 4 && (fy != fz)) sgn = -1.0;
                     for (int kx = 0; kx < p.hx; ++kx) {
-                        const double v = sgn * h[(((size_t)kx * L2 + kyq) * L2 + kzq) * 6 + c];
+                        const double v = sgn * h[(((size_t)kx * Y2 + kyq) * Z2 + kzq) * 6 + c];
                         const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
                         out[2 * o] = v;
                         out[2 * o + 1] = 0.0;
@@ -454,6 +454,10 @@ int mxb_demag_set_fast(mxb_demag* d, int fast) {
     if (!d) { set_error("null argument"); return MXB_EINVAL; }
     if (d->plan.pipe && !fast) {
         set_error("the plane pipeline has no generic path (build the kernel with MXB_PIPE=0)");
+        return MXB_EINVAL;
+    }
+    if (d->plan.longy && !fast) {
+        set_error("the long-y plane-major path has no generic path (build the kernel with MXB_LONGY=0)");
         return MXB_EINVAL;
     }
     d->plan.fast = fast != 0;

@@ -373,6 +373,17 @@ bool DemagPlan::pipe_candidate() const {
     return pz >= 512;
 }
 
+// long y lines beyond the pipeline (py = 2048 / 4096, e.g. the 2048^2 x 64
+// film): plane-major spectra, row kernels for y, the fused z pass over
+// ky-contiguous chunks.  MXB_LONGY=0 keeps the 5-pass column kernels.
+bool DemagPlan::longy_candidate() const {
+    if (G != 1 || pz <= 1 || !fast || pipe) return false;
+    if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
+    if (!longy_shape_ok(py) || !fast_fused_ok(pz)) return false;
+    const char* e = getenv("MXB_LONGY");
+    return !(e && e[0] == '0');
+}
+
 void DemagPlan::release() {
     cudaSetDevice(dev);
     for (auto& t : tw) if (t) cudaFree(t);
@@ -476,6 +487,7 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
     Kc = nullptr;
     kmode = 0;
     pipe = false;
+    longy = false;
     if (Kp) { cudaFree(Kp); Kp = nullptr; }
     if (slots) { cudaFree(slots); slots = nullptr; }
     if (bar) { cudaFree(bar); bar = nullptr; }
@@ -503,6 +515,30 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         cudaFree(K);
         K = nullptr;
         bytes += nk * sizeof(double) + ns * sizeof(double2);
+        has_kernel = true;
+        return MXB_OK;
+    }
+    if (symmetric && longy_candidate()) {
+        // plane-major XR [kx][z][y][3] and X2 [kx][z][ky][3] (both fit the
+        // row-major allocations), kernel Kp[kx][ky'][kz'][6]
+        const size_t nk = (size_t)hx * (py / 2 + 1) * (pz / 2 + 1) * 6;
+        MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
+        int rc = longy_quarter(K, Kp, py, pz, hx, hxp, st);
+        if (rc) return rc;
+        if (!X2) {
+            const size_t x2 = (size_t)g.nz * py * CHP * 3;
+            MXB_CUDA(cudaMalloc(&X2, x2 * sizeof(double2)));
+            bytes += x2 * sizeof(double2);
+        }
+        CH = 1;
+        CHP = 1;
+        blk = (long long)g.nz * g.ny * 3;
+        kmode = 4;
+        longy = true;
+        MXB_CUDA(cudaStreamSynchronize(st));
+        cudaFree(K);
+        K = nullptr;
+        bytes += nk * sizeof(double);
         has_kernel = true;
         return MXB_OK;
     }
@@ -581,6 +617,20 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
         mark(3);
         mark(4);
         return rc;
+    }
+    if (longy) {
+        // y forward (rows (kx, z): ny -> py), fused z over ky-contiguous tiles, y inverse
+        const long long rows = (long long)hx * nz;
+        if ((rc = longy_rows(-1, py, XR, X2, ny, py, rows, ply.tw, st, halt))) return rc;
+        mark(2);
+        FusedArgs a{X2, Kp, nz, (long long)py * 3, py, 0, hx, (long long)nz * py * 3, scale, 1};
+        rc = fast_fused(pz, 4, a, plz.tw, st, halt);
+        if (rc == -1) { set_error("no fused kernel for this shape"); rc = MXB_EINVAL; }
+        if (rc) return rc;
+        mark(3);
+        if ((rc = longy_rows(1, py, X2, XR, py, ny, rows, ply.tw, st, halt))) return rc;
+        mark(4);
+        return MXB_OK;
     }
     auto cols = [&](int dir, const double2* in, double2* out, int n_in, int n_out, long long OS_in,
                     long long OS_out) {

@@ -38,6 +38,11 @@ bool pipe_shape_ok(int ny, int nz);
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
             const double2* tw, cudaStream_t st, const int* halt);
 int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st);
+// long y lines (longy.cu)
+bool longy_shape_ok(int py);
+int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
+               const double2* tw, cudaStream_t st, const int* halt);
+int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st);
 
 struct DemagPlan {
     int dev = 0;
@@ -57,9 +62,10 @@ struct DemagPlan {
     double2* K = nullptr;    // full spectra [pz][py][hxp][6] complex (build scratch)
     double2* Kc = nullptr;   // complex spectra of the chunk [pz][py][CHP][6]
     double* Kq = nullptr;    // parity-reduced real spectra of the chunk [L/2+1][G/2+1][CHP][6]
-    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp
+    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp, 4 long-y Kp
     // plane pipeline (kmode 3): XS is plane-major [kx][z][y][3] (CH = CHP = 1)
     bool pipe = false;
+    bool longy = false;       // plane-major long-y path (longy.cu)
     double* Kp = nullptr;     // [hx][py/2+1][pz/2+1][6]
     double2* slots = nullptr; // 3 x [nz][py][3]
     unsigned* bar = nullptr;
@@ -73,6 +79,7 @@ struct DemagPlan {
 
     int init(const mxb_grid& g, int device, int nranks = 1, int rank = 0);
     bool pipe_candidate() const;
+    bool longy_candidate() const;
     void release();
     int spectra_from_packed_dev(const double* P, cudaStream_t st);
     int spectra_x_component(const double* Pc, int c, cudaStream_t st);

@@ -127,7 +127,9 @@ k_col_direct(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 // ---------------------------------------------------------------------------
 // fused forward * multiply * inverse along the outer axis
 // K storage: KMODE 0 complex [e*G+g][kx][6]; 2 real quarter [e'][g'][kx][6]
-// with e' = min(e, L-e), g' = min(g, G-g) and the parity signs of XY/XZ/YZ.
+// with e' = min(e, L-e), g' = min(g, G-g) and the parity signs of XY/XZ/YZ;
+// 4 (long-y plane-major layout, longy.cu: the contiguous lane is ky, g is kx)
+// real [g][ky'][e'][6] with ky' = min(ky, py-ky), py = a.hx.
 // Tile order pairs g with G-g so the shared quarter rows are reused from L2.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int g_of(int r, int G) {
@@ -140,8 +142,9 @@ __global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, 1)
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
-    constexpr int KROWS = KMODE == 2 ? (L / 2 + 1) : L;
-    constexpr int KCH = KMODE == 2 ? 3 : 6;   // 16-byte chunks per (row, kx)
+    constexpr bool KQ = KMODE == 2 || KMODE == 4;   // real folded kernel
+    constexpr int KROWS = KQ ? (L / 2 + 1) : L;
+    constexpr int KCH = KQ ? 3 : 6;   // 16-byte chunks per (row, kx)
     extern __shared__ double2 sm[];
     double2* X = sm;
     double2* S = X + smem_elems<L, R, NL>();
@@ -171,7 +174,12 @@ k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict_
             const bool ok = kx < a.hx;
             const int kxs = ok ? kx : 0;
             const double2* src;
-            if (KMODE == 2) {
+            if (KMODE == 4) {
+                const int ky2 = 2 * kxs > a.hx ? a.hx - kxs : kxs;
+                src = reinterpret_cast<const double2*>((const double*)a.K +
+                                                       (((long long)g * (a.hx / 2 + 1) + ky2) * KROWS + e) * 6) +
+                      part;
+            } else if (KMODE == 2) {
                 const int g2 = 2 * g > a.G ? a.G - g : g;
                 src = reinterpret_cast<const double2*>((const double*)a.K +
                                                        (((long long)e * G2 + g2) * a.hxp + kxs) * 6) + part;
@@ -215,11 +223,12 @@ k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict_
             const int i0 = sidx<true, L, R, NL>(3 * kl, e);
             const double2 m0 = X[i0], m1 = X[i0 + 1], m2 = X[i0 + 2];
             double2 h0, h1, h2;
-            if (KMODE == 2) {
+            if (KQ) {
                 const bool re = 2 * e > L;
                 const int e2 = re ? L - e : e;
                 const double* k = reinterpret_cast<const double*>(KS + (e2 * NK + kl) * KCH);
-                const bool fy = a.e_is_z ? rg : re, fz = a.e_is_z ? re : rg;
+                const bool fy = KMODE == 4 ? 2 * (kx0 + kl) > a.hx : (a.e_is_z ? rg : re);
+                const bool fz = KMODE == 4 ? re : (a.e_is_z ? re : rg);
                 const double kxx = k[0], kyy = k[3], kzz = k[5];
                 const double kxy = fy ? -k[1] : k[1];
                 const double kxz = fz ? -k[2] : k[2];
@@ -499,8 +508,8 @@ template <int L, int RM>
 static int fused_launch(int kmode, const FusedArgs& a, const double2* tw, cudaStream_t st,
                         const int* halt) {
     constexpr int R = Cfg<L, RM>::R, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
-    const int krows = kmode == 2 ? (L / 2 + 1) : L;
-    const int kch = kmode == 2 ? 3 : 6;
+    const int krows = (kmode == 2 || kmode == 4) ? (L / 2 + 1) : L;
+    const int kch = (kmode == 2 || kmode == 4) ? 3 : 6;
     const size_t sm = ((size_t)smem_elems<L, R, NL>() + (size_t)NL * a.n + (size_t)krows * NK * kch) *
                       sizeof(double2);
     if (sm > kFastSmemMax) return -1;
@@ -510,6 +519,9 @@ static int fused_launch(int kmode, const FusedArgs& a, const double2* tw, cudaSt
     if (kmode == 2) {
         if ((rc = persistent_grid(k_fused_fast<L, 2, RM>, thr, sm, ntiles, &grid))) return rc;
         k_fused_fast<L, 2, RM><<<grid, thr, sm, st>>>(a, tw, halt);
+    } else if (kmode == 4) {
+        if ((rc = persistent_grid(k_fused_fast<L, 4, RM>, thr, sm, ntiles, &grid))) return rc;
+        k_fused_fast<L, 4, RM><<<grid, thr, sm, st>>>(a, tw, halt);
     } else {
         if ((rc = persistent_grid(k_fused_fast<L, 0, RM>, thr, sm, ntiles, &grid))) return rc;
         k_fused_fast<L, 0, RM><<<grid, thr, sm, st>>>(a, tw, halt);

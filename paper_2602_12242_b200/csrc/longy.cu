@@ -1,0 +1,134 @@
+// Long y lines (py = 2048 / 4096, e.g. the 2048 x 2048 x 64 film), single rank.
+//
+// The 5-pass path keeps the spectra row-major, X[z][y][kx][c]: a y column is
+// 16 B every CHP*48 B (98 KB apart at hx = 2049) and two 4096-point lines per
+// CTA need 139 KB of shared memory, so the column passes ran at 18% of HBM.
+// Here the x passes write the plane-major layout of the plane pipeline,
+// XR[kx][z][y][c], so a y line of the three components is one contiguous row:
+//   y forward   k_yrow<L,-1>: row (kx, z) of ny x 48 B -> X2[kx][z][ky][c] (py x 48 B)
+//   z fused     k_fused_fast<pz, 4> over X2 with ky as the contiguous lane
+//               (NK consecutive ky per tile) and the quarter kernel
+//               Kp[kx][ky'][kz'][6] (ky, kz folded; parity signs of XY/XZ/YZ)
+//   y inverse   k_yrow<L,+1>: X2 row (py x 48 B) -> XR row, ny kept
+// One CTA per row: the row is staged with bulk copies into the shared
+// buffer, transformed by the radix-16 CTA core (fft_fast.cuh, the three
+// components as three lines), written back in natural order and stored with
+// one bulk store.
+#include <stdlib.h>
+
+#include "demag.cuh"
+#include "fft_fast.cuh"
+#include "tma.cuh"
+
+namespace mxb {
+
+using namespace ff;
+
+namespace {
+template <int L> struct YRowCfg {
+    static constexpr int R = 16;
+    static constexpr int TPL = L / R;
+    static constexpr int T = 3 * TPL;
+    static constexpr int XE = smem_elems<L, R, 3>();   // exchange buffer, >= 3 L
+};
+constexpr unsigned kChunk = 32768;   // bytes per bulk copy
+}  // namespace
+
+template <int L, int DIR>
+__global__ void __launch_bounds__(YRowCfg<L>::T, 1)
+k_yrow(const double2* __restrict__ in, double2* __restrict__ out, int n_in, int n_out,
+       const double2* __restrict__ tw, const int* __restrict__ halt) {
+    if (halt && *halt) return;
+    constexpr int R = YRowCfg<L>::R, TPL = YRowCfg<L>::TPL;
+    extern __shared__ __align__(128) double2 X[];
+    __shared__ alignas(8) unsigned long long mbar;
+    const long long row = blockIdx.x;
+    const double2* src = in + row * (long long)n_in * 3;
+    double2* dst = out + row * (long long)n_out * 3;
+    const int b = threadIdx.x / TPL, t = threadIdx.x - b * TPL;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar);
+        const unsigned bytes = (unsigned)n_in * 48u;
+        mbar_expect(&mbar, bytes);
+        for (unsigned o = 0; o < bytes; o += kChunk)
+            bulk_g2s_tx(reinterpret_cast<char*>(X) + o, reinterpret_cast<const char*>(src) + o,
+                        bytes - o < kChunk ? bytes - o : kChunk, &mbar);
+    }
+    __syncthreads();
+    mbar_wait(&mbar, 0);
+    double2 v[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        const int e = t + m * TPL;
+        v[m] = e < n_in ? X[e * 3 + b] : make_double2(0.0, 0.0);
+    }
+    fft_core<L, R, 3, false, DIR>(v, X, b, t, tw);   // opens with a barrier
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int e = out_elem<L, R>(t, i);
+        if (e < n_out) X[e * 3 + b] = v[i];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned bytes = (unsigned)n_out * 48u;
+        for (unsigned o = 0; o < bytes; o += kChunk)
+            bulk_s2g(reinterpret_cast<char*>(dst) + o, reinterpret_cast<const char*>(X) + o,
+                     bytes - o < kChunk ? bytes - o : kChunk);
+        bulk_commit();
+        bulk_wait_read();
+    }
+}
+
+template <int L, int DIR>
+static int yrow_launch(const double2* in, double2* out, int n_in, int n_out, long long rows, const double2* tw,
+                       cudaStream_t st, const int* halt) {
+    const size_t smem = (size_t)YRowCfg<L>::XE * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        MXB_CUDA(cudaFuncSetAttribute(k_yrow<L, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_yrow<L, DIR><<<(unsigned)rows, YRowCfg<L>::T, smem, st>>>(in, out, n_in, n_out, tw, halt);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+bool longy_shape_ok(int py) { return py == 2048 || py == 4096; }
+
+int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
+               const double2* tw, cudaStream_t st, const int* halt) {
+    if (L == 2048) return dir < 0 ? yrow_launch<2048, -1>(in, out, n_in, n_out, rows, tw, st, halt)
+                                  : yrow_launch<2048, 1>(in, out, n_in, n_out, rows, tw, st, halt);
+    if (L == 4096) return dir < 0 ? yrow_launch<4096, -1>(in, out, n_in, n_out, rows, tw, st, halt)
+                                  : yrow_launch<4096, 1>(in, out, n_in, n_out, rows, tw, st, halt);
+    set_error("no long-y row kernel for this length");
+    return MXB_EINVAL;
+}
+
+// K (complex full spectra [kz][ky][hxp][6], exactly real) -> Kp[kx][ky'][kz'][6],
+// ky' <= py/2, kz' <= pz/2
+__global__ void k_quarter_kx_major(const double2* __restrict__ K, double* __restrict__ Kp, int py, int pz,
+                                   int hx, int hxp) {
+    const int Y2 = py / 2 + 1, Z2 = pz / 2 + 1;
+    const long long tot = (long long)hx * Y2 * Z2 * 6;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % 6);
+        long long r = i / 6;
+        const int kz = (int)(r % Z2);
+        r /= Z2;
+        const int ky = (int)(r % Y2);
+        const int kx = (int)(r / Y2);
+        Kp[i] = K[(((long long)kz * py + ky) * hxp + kx) * 6 + c].x;
+    }
+}
+
+int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st) {
+    k_quarter_kx_major<<<148 * 8, 256, 0, st>>>(K, Kp, py, pz, hx, hxp);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+}  // namespace mxb
