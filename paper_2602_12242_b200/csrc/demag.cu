@@ -578,6 +578,16 @@ int DemagPlan::x_forward(const double* m, cudaStream_t st, const int* halt) {
     const long long rows = (long long)nz_l * g.ny;
     const int nx = g.nx;
     int rc = -1;
+    static const bool rm_t = !(getenv("MXB_LONGY_RMT") && getenv("MXB_LONGY_RMT")[0] == '0');
+    if (longy && rm_t) {
+        // row-major r2c into X2 (free until the y forward), then a tiled transpose
+        // into the plane-major XR (longy.cu)
+        rc = fast_rows(true, px / 2, m, X2, nullptr, Nl, nx, nx / 2, hx, hxp, (long long)g.nz * g.ny * hxp * 3, rows,
+                       plm.tw, plx.tw, st, halt);
+        if (rc == -1) { set_error("no x kernel for the long-y path"); return MXB_EINVAL; }
+        if (rc) return rc;
+        return longy_rm_to_pm(X2, XS, g.ny, g.nz, hx, hxp, st);
+    }
     if (fast && px >= 4 && (nx % 2) == 0)
         rc = fast_rows(true, px / 2, m, XS, nullptr, Nl, nx, nx / 2, CH, CHP, blk, rows, plm.tw,
                        plx.tw, st, halt);

@@ -43,6 +43,7 @@ bool longy_shape_ok(int py);
 int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
                const double2* tw, cudaStream_t st, const int* halt);
 int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st);
+int longy_rm_to_pm(const double2* in, double2* out, int ny, int nz, int hx, int hxp, cudaStream_t st);
 
 struct DemagPlan {
     int dev = 0;
@@ -95,7 +96,7 @@ struct DemagPlan {
     // dependency guard fired (the field is then invalid)
     int check_abort();
     // kernels one evaluation launches: x forward, the y/z part, x inverse
-    int kernels_per_eval() const { return pipe ? 3 : (pz > 1 && py > 1 ? 5 : 3); }
+    int kernels_per_eval() const { return pipe ? 3 : longy ? 6 : (pz > 1 && py > 1 ? 5 : 3); }
 };
 
 int make_plan(int L, int dev, Plan1D* p, double2** tw_owned);
