@@ -125,6 +125,10 @@ k_col_direct(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+#ifndef MXB_FUSED4_MINB
+#define MXB_FUSED4_MINB 2   // long-y z pass: two CTAs per SM (one at 244 registers)
+#endif
+
 // fused forward * multiply * inverse along the outer axis
 // K storage: KMODE 0 complex [e*G+g][kx][6]; 2 real quarter [e'][g'][kx][6]
 // with e' = min(e, L-e), g' = min(g, G-g) and the parity signs of XY/XZ/YZ;
@@ -138,7 +142,7 @@ __device__ __forceinline__ int g_of(int r, int G) {
 }
 
 template <int L, int KMODE, int RM>
-__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, 1)
+__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, KMODE == 4 ? MXB_FUSED4_MINB : 1)
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
