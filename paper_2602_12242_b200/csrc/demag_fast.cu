@@ -125,9 +125,11 @@ k_col_direct(ColArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-#ifndef MXB_FUSED4_MINB
-#define MXB_FUSED4_MINB 2   // long-y z pass: two CTAs per SM (one at 244 registers)
-#endif
+// CTAs per SM the fused kernels are compiled for: two for the real folded
+// kernel modes up to L = 256 (one CTA at 234-244 registers left the SM at 6
+// warps: long-y z pass at L = 128 38.0 -> 28.0 ms, 5-pass z at L = 128
+// 0.567 -> 0.414 ms, L = 256 -1.6%); one above (L = 1024 would spill 736 B)
+template <int L, int KMODE> constexpr int fused_minb() { return (KMODE == 2 || KMODE == 4) && L <= 256 ? 2 : 1; }
 
 // fused forward * multiply * inverse along the outer axis
 // K storage: KMODE 0 complex [e*G+g][kx][6]; 2 real quarter [e'][g'][kx][6]
@@ -142,7 +144,7 @@ __device__ __forceinline__ int g_of(int r, int G) {
 }
 
 template <int L, int KMODE, int RM>
-__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, KMODE == 4 ? MXB_FUSED4_MINB : 1)
+__global__ void __launch_bounds__(3 * Cfg<L, RM>::NKf * Cfg<L, RM>::TPL, fused_minb<L, KMODE>())
 k_fused_fast(FusedArgs a, const double2* __restrict__ tw, const int* __restrict__ halt) {
     if (halt && *halt) return;
     constexpr int R = Cfg<L, RM>::R, TPL = Cfg<L, RM>::TPL, NK = Cfg<L, RM>::NKf, NL = 3 * NK;
