@@ -412,12 +412,14 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm,
                      "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
                      "peak_source": which, "bytes": "SURVEY 8d fixed formula",
-                     "achieved_impl_bytes": ach_own, "frac_impl_bytes": ach_own / hbm},
+                     "achieved_impl_bytes": ach_own, "frac_impl_bytes": ach_own / hbm,
+                     "frac_vs_8TBs_nominal": ach / 8000.0},
         "step_roofline": {"bytes_per_step": step_bytes,
                           "achieved_GBs": step_bytes / (t_step * 1e-3) / 1e9,
                           "frac": step_bytes / (t_step * 1e-3) / 1e9 / hbm,
                           "bytes_per_step_impl": step_bytes_own,
-                          "frac_impl_bytes": step_bytes_own / (t_step * 1e-3) / 1e9 / hbm},
+                          "frac_impl_bytes": step_bytes_own / (t_step * 1e-3) / 1e9 / hbm,
+                          "frac_vs_8TBs_nominal": step_bytes / (t_step * 1e-3) / 1e9 / 8000.0},
         "kernels_ms_per_step": share,
         "timing": {"repeats": len(runs), "ms_per_step_runs": runs, "statistic": "median",
                    "clock": "CUDA events on the solver stream"},
