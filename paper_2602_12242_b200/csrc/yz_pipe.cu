@@ -45,6 +45,9 @@
 #ifndef MXB_PIPE_W_CTAS
 #define MXB_PIPE_W_CTAS 4
 #endif
+#ifndef MXB_PIPE_LATE_READ_WAIT
+#define MXB_PIPE_LATE_READ_WAIT 1
+#endif
 #ifndef MXB_PIPE_TMA
 #define MXB_PIPE_TMA 1
 #endif
@@ -204,6 +207,11 @@ struct Sched {
             unsigned tg;
             if (dep(u, &c, &tg) && ld_acquire(c) < tg) {
                 if (pending.kind != U_NONE) {
+                    // the pending unit's bulk / TMA stores (async proxy) must have
+                    // completed, not only read shared memory, before consumers see
+                    // its signal (no-op for the cp.async-only kernels)
+                    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
                     signal(pending);
                     pending.kind = U_NONE;
                 }
@@ -443,6 +451,11 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 
     auto stage = [&](const Unit& u) {
         double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
+#if MXB_PIPE_LATE_READ_WAIT
+        // the previous unit's store from W must have read it before this
+        // unit's input lands in W (thread 0 issues both)
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
         if (u.kind == U_A) {
 #if MXB_PIPE_BULK
             if (threadIdx.x == 0)
@@ -517,7 +530,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                          "r"(smem_u32(W)), "r"(3 * ne * 16)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#if !MXB_PIPE_LATE_READ_WAIT
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
         }
 #else
         __syncthreads();
@@ -653,7 +668,10 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                     tma_store_2d(&tmap_slot, cur.idx * 6, y0 + 256, W + 768);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     // W is staged into by the next unit: the stores must have read it
+                    // (waited for in the next stage(), or here)
+#if !MXB_PIPE_LATE_READ_WAIT
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
                 }
 #else
                 __syncthreads();
