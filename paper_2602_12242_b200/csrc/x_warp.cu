@@ -26,6 +26,10 @@ using namespace ff;
 #define MXB_XW_TMA_IN 1   // r2c input rows staged by TMA bulk copies
 #endif
 
+#ifndef MXB_XW_EXIT_READ
+#define MXB_XW_EXIT_READ 1
+#endif
+
 namespace {
 constexpr int XM = 512;          // complex FFT length (px / 2)
 constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
@@ -124,7 +128,13 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
             bulk_s2g(out + ((row0 + 1) * CHP) * 3, W + XHX * 3, XHX * 48);
         }
         bulk_commit();
-        bulk_wait_all();   // complete before the CTA exits (smem is released)
+#if MXB_XW_EXIT_READ
+        // the CTA may exit once the store has read its shared memory; the
+        // global writes complete with the grid (the CTA slot is not held for them)
+        bulk_wait_read();
+#else
+        bulk_wait_all();
+#endif
     }
 }
 
