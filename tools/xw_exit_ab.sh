@@ -1,3 +1,4 @@
+# needs: python tools/build_variant.py xw0 x_warp.cu -DMXB_XW_EXIT_READ=0
 set -x
 python -m pytest tests/test_xwarp.py tests/test_pipe.py -x -q > gpurun_out/xe_tests.txt 2>&1
 for V in xw0 default xw0 default xw0 default; do
