@@ -10,6 +10,8 @@ the stage times, builds sample rows and talks to the caller.
 from __future__ import annotations
 
 import ctypes as C
+import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -289,11 +291,26 @@ class Trajectory:
         mio.write_timeseries_csv(path, self.samples)
 
 
+def _prefault(shape, nthreads: int = 8):
+    """A fresh float64 array whose pages are being written by `nthreads` host
+    threads (ctypes.memset releases the GIL); join the threads before use."""
+    buf = np.empty(shape)
+    n = buf.nbytes
+    step = ((n + nthreads - 1) // nthreads + 4095) // 4096 * 4096
+    threads = []
+    for o in range(0, n, step):
+        th = threading.Thread(target=C.memset, args=(buf.ctypes.data + o, 0, min(step, n - o)), daemon=True)
+        th.start()
+        threads.append(th)
+    return buf, threads
+
+
 class Simulation:
     """Fixed-step driver (llg.py:264-379), device resident."""
 
     CHUNK = 256        # max steps per device launch batch without an equilibrium stop
     CHUNK_EQ = 32      # ... with an equilibrium stop (bounds wasted queued work)
+    PREFAULT_BYTES = 256 << 20   # fault in the final readback array during the run from this size
 
     def __init__(self, state: SimState, rhs: PartitionedRHS, ispec: IntegratorSpec,
                  sample_every: int = 1, sample_callback=None, energy_in_samples: bool = True):
@@ -417,8 +434,21 @@ class Simulation:
         L.check(ctx.call("mxb_state_set", L.dptr(m0)), "state_set")
         grid = state.m.grid
 
+        # the state read back at the end goes into a fresh array; for large grids
+        # its pages are faulted in by host threads while the device steps, so
+        # the final copy runs at copy speed instead of page-fault speed
+        pf_on = os.environ.get("MXB_PREFAULT", "1") != "0"
+        prefault = _prefault((3,) + grid.shape) if pf_on and m0.nbytes >= self.PREFAULT_BYTES else None
+
         def pull():
-            buf = np.empty((3,) + grid.shape)
+            nonlocal prefault
+            if prefault is not None:
+                buf, threads = prefault
+                prefault = None
+                for th in threads:
+                    th.join()
+            else:
+                buf = np.empty((3,) + grid.shape)
             L.check(ctx.call("mxb_state_get", L.dptr(buf)), "state_get")
             state.m = VectorField3(grid, buf)
 

@@ -137,3 +137,14 @@ def test_unpinned_extension_oracles():
     sel = np.abs(m[1, 0, 0, inner]) > 0.5
     expect = (2 * 2e-3 / (mx.MU0 * 8e5 ** 2)) * (np.sin(k * 2e-9) / 2e-9 + 2e-3 / (2 * 1.3e-11))
     assert np.allclose(ratio[sel], expect, rtol=1e-10)
+
+
+def test_prefault_buffer_is_zeroed_fresh_array():
+    # Simulation._run_device faults in its final readback array on host threads
+    from paper_2602_12242_b200.llg import _prefault
+    for shape in [(3, 4, 5, 7), (3, 33, 65, 129)]:
+        buf, threads = _prefault(shape, nthreads=5)
+        for th in threads:
+            th.join()
+        assert buf.shape == shape and buf.dtype == np.float64
+        assert not np.any(buf)
