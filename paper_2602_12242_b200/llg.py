@@ -291,6 +291,10 @@ class Trajectory:
         mio.write_timeseries_csv(path, self.samples)
 
 
+def _zero_range(buf, offset: int, nbytes: int) -> None:
+    C.memset(buf.ctypes.data + offset, 0, nbytes)
+
+
 def _prefault(shape, nthreads: int = 8):
     """A fresh float64 array whose pages are being written by `nthreads` host
     threads (ctypes.memset releases the GIL); join the threads before use."""
@@ -299,7 +303,8 @@ def _prefault(shape, nthreads: int = 8):
     step = ((n + nthreads - 1) // nthreads + 4095) // 4096 * 4096
     threads = []
     for o in range(0, n, step):
-        th = threading.Thread(target=C.memset, args=(buf.ctypes.data + o, 0, min(step, n - o)), daemon=True)
+        # the thread holds `buf` itself, so an abandoned run cannot free it under the memset
+        th = threading.Thread(target=_zero_range, args=(buf, o, min(step, n - o)), daemon=True)
         th.start()
         threads.append(th)
     return buf, threads

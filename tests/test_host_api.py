@@ -148,3 +148,12 @@ def test_prefault_buffer_is_zeroed_fresh_array():
             th.join()
         assert buf.shape == shape and buf.dtype == np.float64
         assert not np.any(buf)
+
+
+def test_prefault_threads_keep_the_buffer_alive():
+    import gc
+    from paper_2602_12242_b200.llg import _prefault
+    _, threads = _prefault((3, 64, 64, 64), nthreads=4)   # buffer dropped at once
+    gc.collect()
+    for th in threads:
+        th.join()
