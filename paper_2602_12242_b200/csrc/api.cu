@@ -392,6 +392,22 @@ int mxb_demag_get_spectra(mxb_demag* d, double* out) {
                     }
         return MXB_OK;
     }
+    if (p.kmode == 5) {
+        // plane-major complex rows Kp[kx][ky][kz][6]
+        const size_t n = (size_t)p.hx * p.py * p.pz * 6;
+        std::vector<double2> h(n);
+        MXB_CUDA(cudaMemcpy(h.data(), p.Kp, n * sizeof(double2), cudaMemcpyDeviceToHost));
+        for (int c = 0; c < 6; ++c)
+            for (int kz = 0; kz < p.pz; ++kz)
+                for (int ky = 0; ky < p.py; ++ky)
+                    for (int kx = 0; kx < p.hx; ++kx) {
+                        const double2 v = h[(((size_t)kx * p.py + ky) * p.pz + kz) * 6 + c];
+                        const size_t o = (((size_t)c * p.pz + kz) * p.py + ky) * p.hx + kx;
+                        out[2 * o] = v.x;
+                        out[2 * o + 1] = v.y;
+                    }
+        return MXB_OK;
+    }
     if (p.kmode == 3 || p.kmode == 4) {
         // plane-major quarter storage Kp[kx][ky'][kz'][6]
         const int Y2 = p.py / 2 + 1, Z2 = p.pz / 2 + 1;

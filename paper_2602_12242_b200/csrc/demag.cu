@@ -361,10 +361,11 @@ int DemagPlan::init(const mxb_grid& gr, int device, int nranks, int rk) {
 
 // shapes the plane pipeline covers (single rank, 3-D, ny == nz, power-of-two
 // padding, fast x rows); MXB_PIPE=0 disables it, MXB_PIPE=1 lifts the size floor
-bool DemagPlan::pipe_candidate() const {
+bool DemagPlan::pipe_candidate(bool symmetric) const {
     if (G != 1 || pz <= 1 || py <= 1 || !fast) return false;
     if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
     if (!pipe_shape_ok(g.ny, g.nz)) return false;
+    if (!symmetric && !pipe_cplx_ok(pz)) return false;
     const char* e = getenv("MXB_PIPE");
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return true;
@@ -496,20 +497,24 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         CHP = hxp;
         blk = (long long)nz_l * g.ny * CHP * 3;
     }
-    if (symmetric && pipe_candidate()) {
-        // plane-major quarter spectra, slot ring, barrier; x passes switch to [kx][z][y][3]
+    if (pipe_candidate(symmetric)) {
+        // plane-major spectra, slot ring, barrier; x passes switch to [kx][z][y][3].
+        // Symmetric (mirrored) tensor: real parity-reduced quarter Kp[kx][ky'][kz'][6];
+        // otherwise (the reference's tensor via from_packed, or the unmirrored GPU
+        // build) the full complex rows Kp[kx][ky][kz][6] (8x the bytes, no symmetry assumed)
         const int L2 = pz / 2 + 1;
-        const size_t nk = (size_t)hx * L2 * L2 * 6;
+        const size_t nk = symmetric ? (size_t)hx * L2 * L2 * 6 : (size_t)hx * pz * pz * 12;
         const size_t ns = (size_t)3 * g.nz * py * 3;
         MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
         MXB_CUDA(cudaMalloc(&slots, ns * sizeof(double2)));
         MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx + 3 * (size_t)g.nz) * sizeof(unsigned)));
-        int rc = pipe_quarter(K, Kp, pz, hx, hxp, st);
+        int rc = symmetric ? pipe_quarter(K, Kp, pz, hx, hxp, st)
+                           : pipe_complex(K, reinterpret_cast<double2*>(Kp), pz, hx, hxp, st);
         if (rc) return rc;
         CH = 1;
         CHP = 1;
         blk = (long long)g.nz * g.ny * 3;
-        kmode = 3;
+        kmode = symmetric ? 3 : 5;
         pipe = true;
         MXB_CUDA(cudaStreamSynchronize(st));
         cudaFree(K);
@@ -623,7 +628,7 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
     if (kxn <= 0) { mark(2); mark(3); mark(4); return MXB_OK; }
     if (pipe) {
         mark(2);
-        rc = pipe_yz(XR, slots, Kp, bar, hx, nz, scale, plz.tw, st, halt);
+        rc = pipe_yz(XR, slots, Kp, bar, hx, nz, scale, plz.tw, st, halt, kmode == 5 ? 1 : 0);
         mark(3);
         mark(4);
         return rc;

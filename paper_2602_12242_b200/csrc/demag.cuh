@@ -36,8 +36,10 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
 // L2-resident y/z pipeline over kx planes (yz_pipe.cu)
 bool pipe_shape_ok(int ny, int nz);
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
-            const double2* tw, cudaStream_t st, const int* halt);
+            const double2* tw, cudaStream_t st, const int* halt, int cplx);
 int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st);
+bool pipe_cplx_ok(int L);
+int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st);
 // long y lines (longy.cu)
 bool longy_shape_ok(int py);
 int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
@@ -63,7 +65,8 @@ struct DemagPlan {
     double2* K = nullptr;    // full spectra [pz][py][hxp][6] complex (build scratch)
     double2* Kc = nullptr;   // complex spectra of the chunk [pz][py][CHP][6]
     double* Kq = nullptr;    // parity-reduced real spectra of the chunk [L/2+1][G/2+1][CHP][6]
-    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp, 4 long-y Kp
+    int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp, 4 long-y Kp,
+                             // 5 plane pipeline with complex spectra (Kp holds [hx][L][L][6] double2)
     // plane pipeline (kmode 3): XS is plane-major [kx][z][y][3] (CH = CHP = 1)
     bool pipe = false;
     bool longy = false;       // plane-major long-y path (longy.cu)
@@ -79,7 +82,7 @@ struct DemagPlan {
     int fused_G() const { return pz > 1 ? py : 1; }
 
     int init(const mxb_grid& g, int device, int nranks = 1, int rank = 0);
-    bool pipe_candidate() const;
+    bool pipe_candidate(bool symmetric = true) const;
     bool longy_candidate() const;
     void release();
     int spectra_from_packed_dev(const double* P, cudaStream_t st);

@@ -72,7 +72,24 @@ struct PipeArgs {
     unsigned* sync;       // [ticket, abort, doneA[hx], doneB[hx], rowgen[3][n]], zeroed per launch
     int hx, n;            // planes; non-zero rows ny == nz == n
     double scale;
+    int cplx;             // 1: Kp holds full complex spectra [hx][L][L][6] (double2), no symmetry assumed
 };
+
+// H = K M for one kz element with complex K (the reference's own tensor, whose
+// spectra are not exactly real): k points at the six complex components
+__device__ __forceinline__ void kmul_complex(const double2* __restrict__ k, double2& m0, double2& m1, double2& m2,
+                                             double s) {
+    const double2 kxx = __ldg(k), kxy = __ldg(k + 1), kxz = __ldg(k + 2);
+    const double2 kyy = __ldg(k + 3), kyz = __ldg(k + 4), kzz = __ldg(k + 5);
+    auto cm = [](double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); };
+    auto ad = [](double2 a, double2 b, double2 c) { return make_double2(a.x + b.x + c.x, a.y + b.y + c.y); };
+    const double2 h0 = ad(cm(kxx, m0), cm(kxy, m1), cm(kxz, m2));
+    const double2 h1 = ad(cm(kxy, m0), cm(kyy, m1), cm(kyz, m2));
+    const double2 h2 = ad(cm(kxz, m0), cm(kyz, m1), cm(kzz, m2));
+    m0 = make_double2(h0.x * s, h0.y * s);
+    m1 = make_double2(h1.x * s, h1.y * s);
+    m2 = make_double2(h2.x * s, h2.y * s);
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -484,9 +501,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             if (threadIdx.x == 0) {
                 // pull the unit's kernel row (L2 x 48 B) into L2 over the forward FFT;
                 // the multiply reads it through the read-only path
-                const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
-                const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+                if (a.cplx) {
+                    const double* kr = a.Kp + ((long long)u.plane * L + u.idx) * L * 12;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L * 96) : "memory");
+                } else {
+                    const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
+                    const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+                }
             }
         } else {
 #if MXB_PIPE_BULK
@@ -613,9 +635,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 __syncthreads();
                 const bool fy = 2 * ky > L;
                 const double s = a.scale;
+                if (a.cplx) {
+                    const double2* krow = Kp2 + ((long long)cur.plane * L + ky) * L * 6;
+                    for (int kz = threadIdx.x; kz < L; kz += 96)
+                        kmul_complex(krow + kz * 6, W[kz], W[L + kz], W[2 * L + kz], s);
+                }
                 const double2* krow = Kp2 + ((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 * 3;
                 // each thread owns whole kz rows (all 3 components), in place in W
-                for (int kz = threadIdx.x; kz < L; kz += 96) {
+                for (int kz = a.cplx ? L : threadIdx.x; kz < L; kz += 96) {
                     const bool fz = 2 * kz > L;
                     const double2* kr = krow + (fz ? L - kz : kz) * 3;
                     const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
@@ -930,8 +957,13 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
             }
             if (threadIdx.x < 2) {
                 const int ky = ky0 + threadIdx.x, kyq = 2 * ky > L ? L - ky : ky;
-                const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+                if (a.cplx) {
+                    const double* kr = a.Kp + ((long long)u.plane * L + ky) * L * 12;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L * 96) : "memory");
+                } else {
+                    const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+                }
             }
         } else {   // slot rows 2 idx, 2 idx + 1: contiguous
             if (threadIdx.x == 0) bulk_g2s(W, slot + (long long)(2 * u.idx) * L * 3, 2 * L * 3 * 16, &mbar);
@@ -1004,7 +1036,14 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
                 for (int k2 = 0; k2 < 32; ++k2) W[c * 1024 + line * L + k1 + 16 * k2] = v[fw::p32(k2)];
                 __syncthreads();
                 const double s = a.scale;
-                for (int t = threadIdx.x; t < 2 * L; t += 96) {
+                if (a.cplx) {
+                    for (int t = threadIdx.x; t < 2 * L; t += 96) {
+                        const int ln = t / L, kz = t - ln * L;
+                        kmul_complex(Kp2 + (((long long)cur.plane * L + ky0 + ln) * L + kz) * 6, W[t], W[1024 + t],
+                                     W[2048 + t], s);
+                    }
+                }
+                for (int t = a.cplx ? 2 * L : threadIdx.x; t < 2 * L; t += 96) {
                     const int ln = t / L, kz = t - ln * L, ky = ky0 + ln;
                     const bool fy = 2 * ky > L, fz = 2 * kz > L;
                     const double2* kr = Kp2 + (((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 +
@@ -1218,9 +1257,19 @@ static int pipe_launch_warp(const PipeArgs& a, const double2* tw, cudaStream_t s
     return MXB_OK;
 }
 
+// the complex-spectra pipeline (the reference's tensor, from_packed) exists for
+// the warp-FFT kernels only
+bool pipe_cplx_ok(int L) {
+    const char* we = getenv("MXB_PIPE_WARP");
+    const char* pe = getenv("MXB_PIPE_PREFETCH");
+    if ((we && we[0] == '0') || (pe && pe[0] == '1')) return false;
+    return L == 512 || L == 1024;
+}
+
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
-            const double2* tw, cudaStream_t st, const int* halt) {
-    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale};
+            const double2* tw, cudaStream_t st, const int* halt, int cplx) {
+    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale, cplx};
+    if (cplx && !pipe_cplx_ok(2 * n)) { set_error("complex-spectra pipeline needs the warp kernels (L = 512 / 1024)"); return MXB_EINVAL; }
     // warp-FFT variant by default at L = 1024 (27.6 vs 32.1 ms per evaluation at
     // 512^3; within 4e-16 of the 5-pass path).  MXB_PIPE_WARP=0 selects the
     // radix-16 pipeline, which is bit-identical to the 5-pass path.
@@ -1263,6 +1312,32 @@ __global__ void k_planes_quarter(const double2* __restrict__ K, double* __restri
 
 int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st) {
     k_planes_quarter<<<148 * 8, 256, 0, st>>>(K, Kp, L, hx, hxp);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
+}  // namespace mxb
+
+namespace mxb {
+
+// K (complex full spectra [kz][ky][hxp][6]) -> Kx[kx][ky][kz][6] complex, the
+// B units' kernel rows contiguous (L x 96 B per (kx, ky))
+__global__ void k_planes_complex(const double2* __restrict__ K, double2* __restrict__ Kx, int L, int hx, int hxp) {
+    const long long tot = (long long)hx * L * L * 6;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % 6);
+        long long r = i / 6;
+        const int kz = (int)(r % L);
+        r /= L;
+        const int ky = (int)(r % L);
+        const int kx = (int)(r / L);
+        Kx[i] = K[(((long long)kz * L + ky) * hxp + kx) * 6 + c];
+    }
+}
+
+int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st) {
+    k_planes_complex<<<148 * 8, 256, 0, st>>>(K, Kx, L, hx, hxp);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }

@@ -96,10 +96,18 @@ class DemagKernel:
 
     @property
     def pipeline(self) -> bool:
-        """True when the y/z passes run as the L2-resident plane pipeline (yz_pipe.cu)."""
+        """True when the y/z passes run as the L2-resident plane pipeline (yz_pipe.cu):
+        kernel mode 3 (mirrored tensor, real quarter spectra) or 5 (any tensor,
+        e.g. the reference's via ``from_packed``: full complex spectra)."""
+        return self.kmode in (3, 5)
+
+    @property
+    def kmode(self) -> int:
+        """Spectra storage: 0 complex (5-pass), 2 real quarter (5-pass), 3 real
+        quarter (plane pipeline), 4 real quarter (long-y), 5 complex (plane pipeline)."""
         k = C.c_int()
         L.check(L.load().mxb_demag_kmode(self._d.h, C.byref(k)), "kmode")
-        return k.value == 3
+        return k.value
 
     def set_fast(self, flag: bool) -> None:
         """Use the register-resident radix-16 kernels (default) or the generic
