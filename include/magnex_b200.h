@@ -185,6 +185,10 @@ typedef struct mxb_run_args {
     uint32_t fast_mask;        /* MRI: terms in the fast partition (llg.py:41-47) */
     int32_t pad;
     double theta;              /* MRI: fast step ratio (IntegratorSpec.theta) */
+    /* host (3,nz,ny,nx) bias fields, one per bias-reading evaluation in the
+     * order of stage_bias (a callable t -> (3,nz,ny,nx) bias, reference
+     * llg.py:92-96,154-164), or NULL; takes precedence over stage_bias */
+    const double* stage_bias_fields;
 } mxb_run_args;
 typedef struct mxb_run_stats {
     int64_t steps_done;        /* committed steps */

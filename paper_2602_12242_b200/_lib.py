@@ -51,7 +51,7 @@ class RunArgs(C.Structure):
     _fields_ = [("method", C.c_int32), ("renorm_each_stage", C.c_int32), ("dt", C.c_double),
                 ("nsteps", C.c_int64), ("eq_tol", C.c_double), ("stage_bias", _dp),
                 ("bias_field", _dp), ("bias_vec", C.c_double * 3), ("fast_mask", C.c_uint32),
-                ("pad", C.c_int32), ("theta", C.c_double)]
+                ("pad", C.c_int32), ("theta", C.c_double), ("stage_bias_fields", _dp)]
 
 
 class StageIO(C.Structure):

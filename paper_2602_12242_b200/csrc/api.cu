@@ -817,7 +817,7 @@ int mxb_state_energies(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_b
 // enqueue one step reading Yb[cur] and writing Yb[cur^1]; stage bias rows
 // `sb` (4 or 1 rows of 3) or the constant a0.bias
 static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int method, double dt,
-                        const double* sb, bool renorm_stage, bool use_demag) {
+                        const double* sb, bool renorm_stage, bool use_demag, const double* sbf = nullptr) {
     const double* y = c->Yb[c->cur];
     double* ynew = c->Yb[c->cur ^ 1];
     const int* halt = &c->ctl->halt;
@@ -830,12 +830,24 @@ static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int metho
     a.hd = c->Hd;
     a.renorm = renorm_stage ? 1 : 0;
     int rc;
+    int brc = MXB_OK;
     auto set_bias = [&](int stage) {
-        if (sb) for (int q = 0; q < 3; ++q) a.bias[q] = sb[3 * stage + q];
+        if (sbf) {
+            // this evaluation's spatial bias field into the scratch buffer (stream-ordered
+            // after the previous stage kernel read it)
+            const size_t fb = fbytes(c->g);
+            cudaError_t e = cudaMemcpyAsync(c->bias_dev, sbf + (size_t)stage * 3 * c->g.N, fb,
+                                            cudaMemcpyHostToDevice, c->st);
+            if (e != cudaSuccess) brc = cuda_fail(e, "stage bias field", __FILE__, __LINE__);
+            a.bias_field = c->bias_dev;
+        } else if (sb) {
+            for (int q = 0; q < 3; ++q) a.bias[q] = sb[3 * stage + q];
+        }
     };
     if (method == MXB_EULER) {
         if (use_demag && (rc = demag_into(c, d, y, c->Hd, halt))) return rc;
         set_bias(0);
+        if (brc) return brc;
         a.ys = y;
         a.out = ynew;
         a.c = dt;
@@ -845,18 +857,22 @@ static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int metho
     // stage 1: y -> P (y2)
     if (use_demag && (rc = demag_into(c, d, y, c->Hd, halt))) return rc;
     set_bias(0); a.ys = y; a.out = c->P; a.c = half;
+    if (brc) return brc;
     if ((rc = launch_stage(M_RK1, c->exact, a, c->st))) return rc;
     // stage 2: P -> ynew (y3)
     if (use_demag && (rc = demag_into(c, d, c->P, c->Hd, halt))) return rc;
     set_bias(1); a.ys = c->P; a.out = ynew; a.c = half;
+    if (brc) return brc;
     if ((rc = launch_stage(M_RK2, c->exact, a, c->st))) return rc;
     // stage 3: ynew (y3) -> P (y4)
     if (use_demag && (rc = demag_into(c, d, ynew, c->Hd, halt))) return rc;
     set_bias(2); a.ys = ynew; a.out = c->P; a.c = dt;
+    if (brc) return brc;
     if ((rc = launch_stage(M_RK3, c->exact, a, c->st))) return rc;
     // stage 4: P (y4) -> ynew
     if (use_demag && (rc = demag_into(c, d, c->P, c->Hd, halt))) return rc;
     set_bias(3); a.ys = c->P; a.out = ynew; a.dt6 = dt / 6.0;
+    if (brc) return brc;
     return launch_stage(M_RK4, c->exact, a, c->st);
 }
 
@@ -878,7 +894,7 @@ int mri_substeps(double theta, int n[3]) {
 
 static int enqueue_step_mri(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, uint32_t mask,
                             uint32_t fast_mask, double dt, double theta, const double* rows,
-                            int* row_i, bool renorm) {
+                            int* row_i, bool renorm, const double* row_fields = nullptr) {
     const uint32_t slow_mask = mask & ~fast_mask;
     const bool bias_fast = (fast_mask & MXB_TERM_BIAS) != 0;
     double* y = c->Yb[c->cur];
@@ -895,7 +911,12 @@ static int enqueue_step_mri(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, uint3
         a.terms = m;
         a.ys = ys;
         a.out = out;
-        if ((m & MXB_TERM_BIAS) && rows && (is_fast == bias_fast)) {
+        if ((m & MXB_TERM_BIAS) && row_fields && (is_fast == bias_fast)) {
+            MXB_CUDA(cudaMemcpyAsync(c->bias_dev, row_fields + (size_t)(*row_i) * 3 * c->g.N, fb,
+                                     cudaMemcpyHostToDevice, c->st));
+            a.bias_field = c->bias_dev;
+            ++*row_i;
+        } else if ((m & MXB_TERM_BIAS) && rows && (is_fast == bias_fast)) {
             for (int q = 0; q < 3; ++q) a.bias[q] = rows[3 * (*row_i) + q];
             ++*row_i;
         }
@@ -997,8 +1018,10 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     a.prec = t->precession;
     a.damp = t->damping;
     for (int q = 0; q < 3; ++q) a.bias[q] = ra->bias_vec[q];
-    if (ra->bias_field) {
+    if (ra->bias_field || ra->stage_bias_fields) {
         if ((rc = ensure(&c->bias_dev, fbytes(c->g)))) return rc;
+    }
+    if (ra->bias_field && !ra->stage_bias_fields) {
         MXB_CUDA(cudaMemcpyAsync(c->bias_dev, ra->bias_field, fbytes(c->g), cudaMemcpyHostToDevice, c->st));
         a.bias_field = c->bias_dev;
     }
@@ -1012,7 +1035,7 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     // constant bias: replay one captured CUDA graph per step (launch-bound small
     // grids); the first step of a configuration runs eagerly (attribute setup)
     static const bool graphs_on = getenv("MXB_GRAPHS") == nullptr || atoi(getenv("MXB_GRAPHS")) != 0;
-    const bool use_graph = graphs_on && !ra->stage_bias;
+    const bool use_graph = graphs_on && !ra->stage_bias && !ra->stage_bias_fields;
     for (int64_t k = 0; k < ra->nsteps; ++k) {
         if (use_graph && k > 0) {
             std::vector<double> key = {(double)t->mask, (double)t->ghost_mode, (double)t->precession,
@@ -1045,10 +1068,12 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
         }
         if (ra->method == MXB_MRI_KW3) {
             rc = enqueue_step_mri(c, d, a, t->mask, ra->fast_mask & t->mask, ra->dt, ra->theta,
-                                  ra->stage_bias, &row_i, ra->renorm_each_stage != 0);
+                                  ra->stage_bias, &row_i, ra->renorm_each_stage != 0, ra->stage_bias_fields);
         } else {
             const double* sb = ra->stage_bias ? ra->stage_bias + (size_t)k * stages * 3 : nullptr;
-            rc = enqueue_step(c, d, a, ra->method, ra->dt, sb, ra->renorm_each_stage != 0, use_demag);
+            const double* sbf = ra->stage_bias_fields
+                                    ? ra->stage_bias_fields + (size_t)k * stages * 3 * c->g.N : nullptr;
+            rc = enqueue_step(c, d, a, ra->method, ra->dt, sb, ra->renorm_each_stage != 0, use_demag, sbf);
         }
         if (rc) return rc;
         c->cur ^= 1;

@@ -6,15 +6,18 @@
 // differences (z, then y, then x; (hi - 2 mid) + lo each), divided by 4*pi,
 // and elements beyond 60 cell diagonals switch to the point-dipole form.
 // Arithmetic runs with explicitly rounded intrinsics (no FMA contraction) in
-// the reference's operation order; the transcendental functions are CUDA's,
-// so values agree with numpy to round-off amplified by the corner-sum
-// cancellation, not bitwise.
+// the reference's operation order, and arcsinh/arctan (and the dipole r^5)
+// are correctly rounded (dd_math.cuh): the lattice values are bitwise the
+// reference's wherever numpy's own results are correctly rounded (all but
+// ~0.4% of the arctan and ~0.03% of the arcsinh arguments); CUDA's
+// asinh/atan (2-3 ulp) moved the field by 5e-10..5e-8 at 32^3..128^3.
 //
 // symmetric=1 evaluates the non-negative displacement octant only and
 // mirrors it with the exact parities (XX,YY,ZZ even; XY odd in x,y; XZ odd in
 // x,z; YZ odd in y,z), which makes the spectra exactly real.
 #include <math.h>
 
+#include "dd_math.cuh"
 #include "demag.cuh"
 
 namespace mxb {
@@ -29,10 +32,10 @@ __device__ double nf(double x, double y, double z) {
     const double r = sqrt(A_(A_(x2, y2), z2));
     const double sxz = sqrt(A_(x2, z2));
     const double sxy = sqrt(A_(x2, y2));
-    const double t1 = M_(M_(M_(0.5, y), S_(z2, x2)), asinh(sxz > 0 ? div_rn(y, sxz) : 0.0));
-    const double t2 = M_(M_(M_(0.5, z), S_(y2, x2)), asinh(sxy > 0 ? div_rn(z, sxy) : 0.0));
+    const double t1 = M_(M_(M_(0.5, y), S_(z2, x2)), ddm::asinh_cr(sxz > 0 ? div_rn(y, sxz) : 0.0));
+    const double t2 = M_(M_(M_(0.5, z), S_(y2, x2)), ddm::asinh_cr(sxy > 0 ? div_rn(z, sxy) : 0.0));
     const double xr = M_(x, r);
-    const double t3 = M_(M_(M_(-x, y), z), atan(xr > 0 ? div_rn(M_(y, z), xr) : 0.0));
+    const double t3 = M_(M_(M_(-x, y), z), ddm::atan_cr(xr > 0 ? div_rn(M_(y, z), xr) : 0.0));
     const double t4 = div_rn(M_(S_(S_(M_(2.0, x2), y2), z2), r), 6.0);
     return A_(A_(A_(t1, t2), t3), t4);
 }
@@ -44,12 +47,12 @@ __device__ double ng(double x, double y, double z) {
     const double x2 = M_(x, x), y2 = M_(y, y), z2 = M_(z, z);
     const double r = sqrt(A_(A_(x2, y2), z2));
     const double sxy = sqrt(A_(x2, y2)), syz = sqrt(A_(y2, z2)), sxz = sqrt(A_(x2, z2));
-    const double t1 = M_(M_(M_(x, y), z), asinh(sdiv(z, sxy)));
-    const double t2 = M_(M_(div_rn(y, 6.0), S_(M_(3.0, z2), y2)), asinh(sdiv(x, syz)));
-    const double t3 = M_(M_(div_rn(x, 6.0), S_(M_(3.0, z2), x2)), asinh(sdiv(y, sxz)));
-    const double t4 = M_(-div_rn(M_(z2, z), 6.0), atan(sdiv(M_(x, y), M_(z, r))));
-    const double t5 = M_(-div_rn(M_(z, y2), 2.0), atan(sdiv(M_(x, z), M_(y, r))));
-    const double t6 = M_(-div_rn(M_(z, x2), 2.0), atan(sdiv(M_(y, z), M_(x, r))));
+    const double t1 = M_(M_(M_(x, y), z), ddm::asinh_cr(sdiv(z, sxy)));
+    const double t2 = M_(M_(div_rn(y, 6.0), S_(M_(3.0, z2), y2)), ddm::asinh_cr(sdiv(x, syz)));
+    const double t3 = M_(M_(div_rn(x, 6.0), S_(M_(3.0, z2), x2)), ddm::asinh_cr(sdiv(y, sxz)));
+    const double t4 = M_(-div_rn(M_(z2, z), 6.0), ddm::atan_cr(sdiv(M_(x, y), M_(z, r))));
+    const double t5 = M_(-div_rn(M_(z, y2), 2.0), ddm::atan_cr(sdiv(M_(x, z), M_(y, r))));
+    const double t6 = M_(-div_rn(M_(z, x2), 2.0), ddm::atan_cr(sdiv(M_(y, z), M_(x, r))));
     const double t7 = div_rn(M_(M_(-x, y), r), 3.0);
     return A_(A_(A_(A_(A_(A_(t1, t2), t3), t4), t5), t6), t7);
 }
@@ -89,7 +92,7 @@ __device__ double element(const double* F, int comp, int nx, int ny, int nz, int
     const double r2 = A_(A_(M_(X, X), M_(Y, Y)), M_(Z, Z));
     const double c = div_rn(1.0, M_(4.0, 3.141592653589793));
     if (r2 > far2) {
-        const double r5 = pow(r2, 2.5);
+        const double r5 = ddm::pow25_cr(r2);
         switch (comp) {
             case 0: return div_rn(M_(c, S_(M_(M_(3.0, X), X), r2)), r5);
             case 3: return div_rn(M_(c, S_(M_(M_(3.0, Y), Y), r2)), r5);

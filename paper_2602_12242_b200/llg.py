@@ -316,6 +316,7 @@ class Simulation:
     CHUNK = 256        # max steps per device launch batch without an equilibrium stop
     CHUNK_EQ = 32      # ... with an equilibrium stop (bounds wasted queued work)
     PREFAULT_BYTES = 256 << 20   # fault in the final readback array during the run from this size
+    STAGE_FIELD_BYTES = 256 << 20   # host bias fields per device chunk (callable spatial bias)
 
     def __init__(self, state: SimState, rhs: PartitionedRHS, ispec: IntegratorSpec,
                  sample_every: int = 1, sample_callback=None, energy_in_samples: bool = True):
@@ -497,17 +498,36 @@ class Simulation:
         k = 0
         equilibrated = False
         stats = L.RunStats()
+        # a callable bias returning (3,nz,ny,nx) fields (reference llg.py:92-96,154-164;
+        # scenario.build_bias returns one for every spatial expression): one field per
+        # bias-reading evaluation is uploaded before that evaluation; chunks are sized
+        # so the host fields of one chunk stay under STAGE_FIELD_BYTES
+        spatial = callable(rhs._bias) and np.shape(rhs.bias_at(t0)) != (3,)
+        n_bias = max(len(self._bias_times(t0)), 1)
+        field_chunk = max(1, self.STAGE_FIELD_BYTES // (n_bias * 24 * grid.n_cells))
         while k < n_total:
             to_sample = self.sample_every - (k % self.sample_every)
             chunk = min(n_total - k, to_sample, self.CHUNK_EQ if eq is not None else self.CHUNK)
-            if callable(rhs._bias):
+            args.stage_bias_fields = None
+            if spatial:
+                chunk = min(chunk, field_chunk)
+                flds = np.empty((chunk * n_bias, 3) + grid.shape)
+                i = 0
+                for s in range(chunk):
+                    for tt in self._bias_times(t0 + (k + s) * sp.dt):
+                        v = rhs.bias_at(tt)
+                        flds[i] = v[:, None, None, None] if v.shape == (3,) else v
+                        i += 1
+                args.stage_bias_fields = L.dptr(flds)
+                args.stage_bias = None
+                keep_sbf = flds  # noqa: F841 (kept alive during the call)
+            elif callable(rhs._bias):
                 rows = []
                 for s in range(chunk):
                     for tt in self._bias_times(t0 + (k + s) * sp.dt):
                         v = rhs.bias_at(tt)
                         if v.shape != (3,):
-                            raise NotImplementedError(
-                                "time-dependent spatial bias fields are not supported by the device loop")
+                            raise ValueError("a bias callable must return the same shape at every t")
                         rows.append(v)
                 sb = np.ascontiguousarray(np.array(rows, dtype=np.float64))
                 args.stage_bias = L.dptr(sb)

@@ -113,7 +113,124 @@ def disk(g):
     return np.where((X - cx) ** 2 + (Y - cx) ** 2 <= R * R, 1.1e6, 0.0)
 
 
+SPATIAL_SCENARIO = """\
+[grid]
+nx = 12
+ny = 10
+nz = 2
+dx = 2e-9
+dy = 2e-9
+dz = 2e-9
+[material]
+ms = 8e5
+aex = 1.3e-11
+alpha = 0.1
+ku = 3e4
+[physics]
+exchange = true
+demag = true
+anisotropy = true
+[bias]
+hx = "2e4 * sin(2 * pi * x / 24e-9) * cos(2 * pi * t / 5e-13)"
+hy = "where(y > 10e-9, 5e3, -5e3)"
+hz = "1e4 * exp(-t / 2e-13) + 1e3 * z / 4e-9"
+[initial]
+mx = "cos(x / 6e-9)"
+my = "sin(x / 6e-9)"
+mz = "0.2"
+[integrator]
+method = rk4
+dt = 1e-14
+[stop]
+max_steps = 20
+[output]
+sample_every = 1
+energies = true
+"""
+
+
+def spatial_bias_golden():
+    """A scenario whose bias is a spatial, time-dependent expression: the
+    reference's ScenarioConfig.build_bias returns t -> (3,nz,ny,nx)
+    (scenario.py:442-465).  The bias field of every stage evaluation is
+    recorded (so the test can replay it bit for bit) with the run's trace."""
+    from magnex.scenario import loads
+    out = {}
+    for method, dt in (("rk4", 1e-14), ("euler", 5e-15)):
+        cfg = loads(SPATIAL_SCENARIO.replace("method = rk4", f"method = {method}")
+                    .replace("dt = 1e-14", f"dt = {dt!r}"))
+        sim = cfg.build_simulation()
+        bias = sim.rhs._bias
+        assert callable(bias)
+        seen = {}
+
+        def rec(t, _b=bias, _seen=seen):
+            v = _b(t)
+            _seen.setdefault(float(t), v.copy())
+            return v
+
+        sim.rhs._bias = rec
+        m0 = sim.state.m.data.copy()
+        tr = sim.run_until(cfg.stop)
+        ts = np.array(sorted(seen))
+        out[method + "_m0"] = m0
+        out[method + "_times"] = ts
+        out[method + "_fields"] = np.stack([seen[t] for t in ts])
+        out[method + "_mean"] = np.stack([tr.column("mx"), tr.column("my"), tr.column("mz")], 1)
+        out[method + "_e_total"] = tr.column("e_total")
+        out[method + "_final"] = sim.state.m.data.copy()
+        out[method + "_dt"] = dt
+    mat = loads(SPATIAL_SCENARIO).build_material()
+    out["Ms"], out["A"], out["Ku"], out["alpha"], out["eK"] = mat.Ms, mat.A, mat.Ku, mat.alpha, mat.eK
+    out["scenario"] = np.array(SPATIAL_SCENARIO)
+    np.savez_compressed(os.path.join(OUT, "spatial_bias.npz"), **out)
+    print("spatial_bias ok", out["rk4_fields"].shape)
+
+
+def sp4_protocol_golden():
+    """muMAG SP4 field 1 on the reference's coarse grid (160x40x1, 3.125 nm,
+    padded 320x80: radix 5) through the reference's own driver: S-state
+    preparation with ramped_bias at alpha = 0.5 (30 ps + relaxation up to
+    1 ns at the equilibrium tolerance), then 2 ns of field 1 at alpha = 0.02
+    with energy samples every ~1 ps (bench/std4.py:67-188) and crossing_time
+    (bench/std4.py:191-200)."""
+    from magnex.bench import std4
+    p = std4.Std4Params()
+    s_state = std4.prepare_s_state("coarse", p, emit=print)
+    res, checks = std4.run_std4(1, "coarse", p, s_state=s_state, emit=print)
+    tr = res.trajectory
+    np.savez_compressed(os.path.join(OUT, "sp4_protocol.npz"),
+                        s_state=s_state.data, t=tr.column("t"), mx=tr.column("mx"),
+                        my=tr.column("my"), mz=tr.column("mz"), e_total=tr.column("e_total"),
+                        e_demag=tr.column("e_demag"), e_exch=tr.column("e_exch"),
+                        n_demag=tr.column("n_demag_evals"),
+                        crossing_time=np.nan if res.crossing_time is None else res.crossing_time,
+                        stop_reason=np.array(tr.stop_reason),
+                        numpy=np.__version__, scipy=scipy.__version__)
+    print("sp4_protocol ok, crossing", res.crossing_time, "samples", len(tr.samples))
+
+
+def radix5_goldens():
+    """Padded lengths with a factor 5 (2n padding, demag.py:152-155): the
+    100x100 DMI disk with demag (skyrmion benchmark, 200x200) and the SP4
+    coarse grid (160x40x1 -> 320x80)."""
+    ALL = ("exchange", "anisotropy", "dmi")
+    case("dmi_disk_100_demag", (100, 100, 1), (1e-9, 1e-9, 0.25e-9),
+         dict(A=16e-12, Ku=5.5e5, D=4.5e-3, alpha=1.0), ALL, 16, msmap=disk, demag=True,
+         dt=1e-14, nsteps=10, store_tensor=False)
+    d = 3.125e-9
+    case("sp4_160x40x1", (160, 40, 1), (d, d, 3e-9),
+         dict(Ms=8e5, A=1.3e-11, alpha=0.02), ("exchange",), 17,
+         bias=(-19576.0, 3422.0, 0.0), demag=True, dt=2e-13, nsteps=20, store_tensor=False)
+
+
 def main():
+    groups = sys.argv[1:]
+    if groups:
+        for gname in groups:
+            {"spatial": spatial_bias_golden, "sp4_protocol": sp4_protocol_golden,
+             "radix5": radix5_goldens}[gname]()
+        return
     ALL = ("exchange", "anisotropy", "dmi")
     # tiny grids: every term, every boundary mode
     case("box_6x5x4_all", (6, 5, 4), (1e-9, 2e-9, 1.5e-9),
@@ -198,6 +315,9 @@ def main():
                         n_demag=tr.column("n_demag_evals"),
                         final_sha=sha(st.m.data), mean_final=mean_normalized(st.m, mat))
     print("sp4_trace ok, dt", dt, "final mean", mean_normalized(st.m, mat))
+    radix5_goldens()
+    spatial_bias_golden()
+    sp4_protocol_golden()
 
 
 if __name__ == "__main__":

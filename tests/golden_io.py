@@ -9,7 +9,8 @@ from oracle import magnex_oracle as O
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-               if not os.path.basename(p).startswith(("tensor_known", "sp4_trace", "fno_")))
+               if not os.path.basename(p).startswith(("tensor_known", "sp4_trace", "fno_", "spatial_bias",
+                                                           "sp4_protocol")))
 
 
 def load(name):
@@ -33,3 +34,31 @@ def packed_of(z):
     nx, ny, nz = (int(v) for v in z["dims"])
     dx, dy, dz = (float(v) for v in z["cell"])
     return O.packed_tensor(nx, ny, nz, dx, dy, dz)
+
+
+class BiasReplay:
+    """t -> the recorded (3,nz,ny,nx) bias field of the reference run at t
+    (tests/golden/make_golden.py spatial_bias_golden): the reference's
+    ScenarioConfig.build_bias callable, replayed bit for bit.  Stage times are
+    matched to the nearest recorded time (|dt| <= 1e-9 of the step)."""
+
+    def __init__(self, times, fields, dt):
+        self.times = np.asarray(times)
+        self.fields = fields
+        self.tol = 1e-9 * dt
+
+    def __call__(self, t):
+        i = int(np.argmin(np.abs(self.times - t)))
+        if abs(self.times[i] - t) > self.tol:
+            raise KeyError(f"no recorded bias at t = {t!r}")
+        return self.fields[i].copy()
+
+
+def spatial_case(method):
+    z = load("spatial_bias")
+    Ms = z["Ms"]
+    nz, ny, nx = Ms.shape
+    mat = O.Mat((nx, ny, nz), (2e-9, 2e-9, 2e-9), Ms, z["A"], z["Ku"], np.zeros_like(Ms),
+                z["alpha"], z["eK"])
+    dt = float(z[method + "_dt"])
+    return z, mat, dt, BiasReplay(z[method + "_times"], z[method + "_fields"], dt)

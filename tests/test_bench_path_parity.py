@@ -127,11 +127,13 @@ def test_complex_pipeline_rk4_run_matches_oracle():
     assert e <= 1e-12
 
 
-# measured on B200 (round 2, printed by the test): the GPU-built tensor against
-# the reference tensor, for a random-direction m (the bench's state).  The
-# mirrored build (bench) and the unmirrored build (API default) differ from the
-# reference by the same order: the reference's own libm-level noise floor.
-SYM_DEV = {32: 2e-10, 64: 2e-9, 128: 4e-9}
+# The GPU-built tensor against the reference tensor, random-direction m (the
+# bench's state), measured on B200 and printed by the test.  The mirrored build
+# (bench) and the unmirrored build (API default) sit at the reference's own
+# reproducibility floor: numpy's arcsinh on a non-AVX-512 host (glibc instead of
+# SVML) moves the reference's field by 4.0e-10 at 32^3 and 8.6e-9 at 64^3
+# (tests/test_tensor_noise_floor.py).
+SYM_DEV = {32: 1e-10, 64: 2e-9, 128: 1e-8}
 
 
 @pytest.mark.parametrize("n", [32, 64, 128])

@@ -111,7 +111,8 @@ def test_magf_and_csv_roundtrip(tmp_path):
 
 def test_unpinned_extension_oracles():
     """Cubic anisotropy and bulk DMI (no reference implementation): analytic checks
-    of the CPU restatements the GPU kernels are tested against."""
+    of the CPU restatements.  The device kernels are compared with these
+    restatements, and checked analytically, in tests/test_gpu_extensions.py."""
     dims, cell = (4, 4, 4), (2e-9,) * 3
     for K1, easy in ((4e4, np.array([1.0, 0.0, 0.0])), (-4e4, np.ones(3) / np.sqrt(3))):
         mat = O.make_mat(dims, cell, 8e5, Kc1=K1)

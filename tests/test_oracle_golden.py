@@ -113,3 +113,37 @@ def test_mri_trace_bit_exact(name):
     got = np.array([[row["mx"], row["my"], row["mz"]] for row in r.rows])
     assert np.array_equal(got, z["mri_trace_m"])
     assert np.array_equal(r.m, z["mri_final"])
+
+
+@pytest.mark.parametrize("method", ["rk4", "euler"])
+def test_spatial_time_dependent_bias_run(method):
+    """The scenario with a spatial, time-dependent bias expression (reference
+    scenario.py:442-465 returns t -> (3,nz,ny,nx)), through the run loop with
+    energies in the samples, vs the reference run."""
+    from tests.golden_io import spatial_case
+    z, mat, dt, bias = spatial_case(method)
+    nx, ny, nz = mat.dims
+    spectra = O.kernel_spectra(O.packed_tensor(nx, ny, nz, 2e-9, 2e-9, 2e-9))
+    terms = O.Terms(exchange=True, anisotropy=True, spectra=spectra, bias=bias)
+    r = O.run(z[method + "_m0"], mat, terms, method, dt, max_steps=20, sample_every=1,
+              with_energies=True)
+    got = np.array([[row["mx"], row["my"], row["mz"]] for row in r.rows])
+    assert np.array_equal(got, z[method + "_mean"])
+    assert np.array_equal(np.array([row["e_total"] for row in r.rows]), z[method + "_e_total"])
+    assert np.array_equal(r.m, z[method + "_final"])
+
+
+def test_sp4_protocol_head():
+    """First 200 field-1 steps of the reference's SP4 coarse protocol
+    (bench/std4.py:124-188) from its S-state, sampled like run_std4 (every
+    5 steps, energies on), vs the reference's recorded samples."""
+    z = load("sp4_protocol")
+    d = 3.125e-9
+    mat = O.make_mat((160, 40, 1), (d, d, d), 8e5, A=1.3e-11, alpha=0.02)
+    spectra = O.kernel_spectra(O.packed_tensor(160, 40, 1, d, d, d))
+    terms = O.Terms(exchange=True, spectra=spectra, bias=np.array([-19576.0, 3422.0, 0.0]))
+    dt = O.stable_dt(d, 1.3e-11, 8e5)
+    r = O.run(z["s_state"], mat, terms, "rk4", dt, max_steps=200, sample_every=5, with_energies=True)
+    n = len(r.rows)
+    for k in ("t", "mx", "my", "mz", "e_total"):
+        assert np.array_equal(np.array([row[k] for row in r.rows]), z[k][:n]), k

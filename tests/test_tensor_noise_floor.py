@@ -21,6 +21,7 @@ H_demag is not defined more tightly than this across libm implementations.
 The GPU-built tensor's measured deviation (tests/test_bench_path_parity.py,
 DESIGN.md section 6) sits at this floor.
 """
+import math
 import types
 
 import numpy as np
@@ -49,6 +50,18 @@ def mirror(n6):
                     ix = np.arange(q.shape[2]) * sx + cx
                     out[c][np.ix_(iz, iy, ix)] = s * q
     return out
+
+
+def tensor_with(dims, cell, atan, asinh):
+    fake = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np) if not k.startswith("__")})
+    fake.arctan = atan
+    fake.arcsinh = asinh
+    real = O.np
+    O.np = fake
+    try:
+        return O.tensor_elements(*dims, *cell)
+    finally:
+        O.np = real
 
 
 def perturbed_tensor(dims, cell, p, seed):
@@ -95,3 +108,24 @@ def test_reference_field_noise_floor():
     # ... by comparable amounts (measured here 2.8e-11 and 5.6e-11 for unit-length
     # random m at 32^3; 4.8e-10 and 1.3e-9 at 64^3 for normal-distributed m)
     assert e_mirror < 1e-9 and e_libm < 1e-9
+
+
+def test_reference_field_across_libms():
+    """The reference on another CPU: numpy's arcsinh/arctan use SVML on
+    AVX-512 hosts and glibc otherwise; glibc's asinh differs from numpy's
+    (AVX-512) in ~20% of arguments here.  The reference's field with glibc's
+    functions (measured 4.0e-10 at 32^3, 8.6e-9 at 64^3 on this AVX-512 host)
+    is the cross-host reproducibility of the reference itself."""
+    dims, cell = (32, 32, 32), (4e-9, 4e-9, 4e-9)
+    n6 = O.tensor_elements(*dims, *cell)
+    fa, fs = np.frompyfunc(math.atan, 1, 1), np.frompyfunc(math.asinh, 1, 1)
+    g6 = tensor_with(dims, cell, lambda v: fa(v).astype(float), lambda v: fs(v).astype(float))
+    m = np.random.default_rng(25).standard_normal((3,) + dims[::-1])
+    m *= 8e5 / np.sqrt((m * m).sum(axis=0))
+
+    def field(t):
+        return O.demag_field(O.kernel_spectra(O.pack_wraparound(t, *dims)), m)
+
+    e = rel(field(g6), field(n6))
+    print(f"32^3: reference field with glibc atan/asinh vs numpy's: {e:.3e}")
+    assert e < 1e-8
