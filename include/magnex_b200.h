@@ -125,6 +125,11 @@ int mxb_demag_build(mxb_demag* d, int symmetric);
 /* real-space tensor_elements (demag.py:90-120) from the GPU builder, host
  * (6, 2nz-1, 2ny-1, 2nx-1) */
 int mxb_demag_tensor_elements(mxb_demag* d, double* out);
+/* demag_field_direct (demag.py:225-248): O(N^2) direct sum over the source
+ * cells of host m (3,nz,ny,nx) into host h, with the tensor elements n6
+ * (6, 2nz-1, 2ny-1, 2nx-1) or, when n6 is NULL, the GPU builder's; the caller
+ * enforces the reference's DIRECT_SUM_CELL_LIMIT */
+int mxb_demag_direct(mxb_demag* d, const double* n6, const double* m, double* h);
 /* DemagKernel.spectra (demag.py:179): host complex (6,pz,py,px/2+1) as
  * interleaved re/im doubles (unscaled, like scipy.fft.rfftn) */
 int mxb_demag_get_spectra(mxb_demag* d, double* out);

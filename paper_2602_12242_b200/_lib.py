@@ -82,6 +82,7 @@ SIGNATURES = {
     "mxb_demag_set_packed": ([C.c_void_p, _dp], C.c_int),
     "mxb_demag_build": ([C.c_void_p, C.c_int], C.c_int),
     "mxb_demag_tensor_elements": ([C.c_void_p, _dp], C.c_int),
+    "mxb_demag_direct": ([C.c_void_p, _dp, _dp, _dp], C.c_int),
     "mxb_demag_get_spectra": ([C.c_void_p, _dp], C.c_int),
     "mxb_demag_field": ([C.c_void_p, _dp, _dp], C.c_int),
     "mxb_demag_field_dev": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

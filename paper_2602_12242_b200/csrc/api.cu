@@ -370,6 +370,41 @@ int mxb_demag_tensor_elements(mxb_demag* d, double* out) {
     return rc;
 }
 
+int mxb_demag_direct(mxb_demag* d, const double* n6_host, const double* m_host, double* h_host) {
+    if (!d || !m_host || !h_host) { set_error("null argument"); return MXB_EINVAL; }
+    DemagPlan& p = d->plan;
+    cudaSetDevice(p.dev);
+    const Grid& g = p.g;
+    const size_t per = (size_t)(2 * g.nx - 1) * (2 * g.ny - 1) * (2 * g.nz - 1);
+    const size_t fb = 3 * (size_t)g.N * sizeof(double);
+    double *E = nullptr, *F = nullptr, *M = nullptr, *H = nullptr;
+    int rc = MXB_OK;
+    auto fail = [&](cudaError_t e, const char* what) { rc = cuda_fail(e, what, __FILE__, __LINE__); };
+    cudaError_t e;
+    if ((e = cudaMalloc(&E, 6 * per * sizeof(double))) != cudaSuccess) fail(e, "alloc");
+    if (!rc && (e = cudaMalloc(&M, fb)) != cudaSuccess) fail(e, "alloc");
+    if (!rc && (e = cudaMalloc(&H, fb)) != cudaSuccess) fail(e, "alloc");
+    if (!rc) {
+        if (n6_host) {
+            if ((e = cudaMemcpyAsync(E, n6_host, 6 * per * sizeof(double), cudaMemcpyHostToDevice, d->st)))
+                fail(e, "copy");
+        } else {
+            const size_t lat = (size_t)(2 * g.nx + 1) * (2 * g.ny + 1) * (2 * g.nz + 1);
+            if ((e = cudaMalloc(&F, lat * sizeof(double))) != cudaSuccess) fail(e, "alloc");
+            else rc = newell_elements(g, E, F, d->st);
+        }
+    }
+    if (!rc && (e = cudaMemcpyAsync(M, m_host, fb, cudaMemcpyHostToDevice, d->st))) fail(e, "copy");
+    if (!rc) rc = direct_sum(g, E, M, H, d->st);
+    if (!rc && (e = cudaMemcpyAsync(h_host, H, fb, cudaMemcpyDeviceToHost, d->st))) fail(e, "copy");
+    cudaStreamSynchronize(d->st);
+    cudaFree(E);
+    cudaFree(F);
+    cudaFree(M);
+    cudaFree(H);
+    return rc;
+}
+
 int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     if (!d || !out) { set_error("null argument"); return MXB_EINVAL; }
     DemagPlan& p = d->plan;
@@ -982,6 +1017,8 @@ static int enqueue_step_mri(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, uint3
     return launch_final_state(c->exact, a, V, ynew, c->st);
 }
 
+static const size_t kMaxGraphs = 8;   // cached step graphs per context (LRU)
+
 int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra,
             mxb_run_stats* st) {
     if (!c || !t || !ra || !st) { set_error("null argument"); return MXB_EINVAL; }
@@ -1044,8 +1081,13 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
                                        a.bias[0], a.bias[1], a.bias[2], (double)(uintptr_t)a.bias_field,
                                        (double)(d ? d->uid : 0), (double)ra->fast_mask};
             cudaGraphExec_t ex = nullptr;
-            for (auto& gr : c->graphs)
-                if (gr.key == key) { ex = gr.exec; break; }
+            for (size_t gi = 0; gi < c->graphs.size(); ++gi)
+                if (c->graphs[gi].key == key) {
+                    ex = c->graphs[gi].exec;
+                    // most recently used last (the front is evicted first)
+                    std::rotate(c->graphs.begin() + gi, c->graphs.begin() + gi + 1, c->graphs.end());
+                    break;
+                }
             if (!ex) {
                 MXB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
                 int crc = ra->method == MXB_MRI_KW3
@@ -1060,6 +1102,13 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
                 e = cudaGraphInstantiate(&ex, gr, 0);
                 cudaGraphDestroy(gr);
                 if (e != cudaSuccess) return cuda_fail(e, "graph instantiate", __FILE__, __LINE__);
+                // bounded cache: a field sweep (set_bias per point) must not keep
+                // one instantiated graph per point alive
+                if (c->graphs.size() >= kMaxGraphs) {
+                    MXB_CUDA(cudaStreamSynchronize(c->st));
+                    cudaGraphExecDestroy(c->graphs.front().exec);
+                    c->graphs.erase(c->graphs.begin());
+                }
                 c->graphs.push_back({key, ex});
             }
             MXB_CUDA(cudaGraphLaunch(ex, c->st));

@@ -114,5 +114,6 @@ int launch_lines(int dir, const Plan1D& p, const double2* in, double2* out, int 
 int newell_packed_component(const Grid& g, int comp, int symmetric, double* packed_c,
                             double* lattice_scratch, cudaStream_t st);
 int newell_elements(const Grid& g, double* out6, double* lattice_scratch, cudaStream_t st);
+int direct_sum(const Grid& g, const double* n6, const double* m, double* h, cudaStream_t st);
 
 }  // namespace mxb

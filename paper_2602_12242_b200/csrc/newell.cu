@@ -218,4 +218,46 @@ int newell_elements(const Grid& g, double* out6, double* lattice, cudaStream_t s
     return MXB_OK;
 }
 
+// O(N^2) direct sum over source cells (demag_field_direct, demag.py:225-248):
+// one thread per target cell, sources in the reference's order (qz, qy, qx),
+// zero-magnetisation sources skipped, each source's contribution formed as
+// (N_a0 m0 + N_a1 m1) + N_a2 m2 and accumulated with explicit rounding, so
+// the sum is the reference's operation for operation.  n6 in the
+// tensor_elements layout (6, 2nz-1, 2ny-1, 2nx-1).
+__global__ void k_direct_sum(const double* __restrict__ n6, const double* __restrict__ m,
+                             double* __restrict__ h, int nx, int ny, int nz) {
+    const long long N = (long long)nx * ny * nz;
+    const long long ex = 2 * nx - 1, ey = 2 * ny - 1, per = ex * ey * (2 * nz - 1);
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int px = (int)(t % nx), py = (int)((t / nx) % ny), pz = (int)(t / ((long long)nx * ny));
+    const int mix[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int qz = 0; qz < nz; ++qz)
+        for (int qy = 0; qy < ny; ++qy)
+            for (int qx = 0; qx < nx; ++qx) {
+                const long long q = ((long long)qz * ny + qy) * nx + qx;
+                const double m0 = m[q], m1 = m[N + q], m2 = m[2 * N + q];
+                if (m0 == 0.0 && m1 == 0.0 && m2 == 0.0) continue;
+                const long long e = ((long long)(nz - 1 - qz + pz) * ey + (ny - 1 - qy + py)) * ex +
+                                    (nx - 1 - qx + px);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const double v = A_(A_(M_(n6[mix[a][0] * per + e], m0), M_(n6[mix[a][1] * per + e], m1)),
+                                        M_(n6[mix[a][2] * per + e], m2));
+                    acc[a] = A_(acc[a], v);
+                }
+            }
+    h[t] = acc[0];
+    h[N + t] = acc[1];
+    h[2 * N + t] = acc[2];
+}
+
+int direct_sum(const Grid& g, const double* n6, const double* m, double* h, cudaStream_t st) {
+    const long long N = g.N;
+    k_direct_sum<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(n6, m, h, g.nx, g.ny, g.nz);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
 }  // namespace mxb

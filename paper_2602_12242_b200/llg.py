@@ -444,7 +444,10 @@ class Simulation:
         # its pages are faulted in by host threads while the device steps, so
         # the final copy runs at copy speed instead of page-fault speed
         pf_on = os.environ.get("MXB_PREFAULT", "1") != "0"
-        prefault = _prefault((3,) + grid.shape) if pf_on and m0.nbytes >= self.PREFAULT_BYTES else None
+        # (a sample callback pulls the state at every sample, so the buffer would
+        # be used up at t = 0: prefault only runs without one)
+        prefault = (_prefault((3,) + grid.shape) if pf_on and m0.nbytes >= self.PREFAULT_BYTES
+                    and self.sample_callback is None else None)
 
         def pull():
             nonlocal prefault
@@ -502,8 +505,17 @@ class Simulation:
         # scenario.build_bias returns one for every spatial expression): one field per
         # bias-reading evaluation is uploaded before that evaluation; chunks are sized
         # so the host fields of one chunk stay under STAGE_FIELD_BYTES
-        spatial = callable(rhs._bias) and np.shape(rhs.bias_at(t0)) != (3,)
+        probe = {}   # the shape probe at the first stage time is reused, not re-evaluated
+        if callable(rhs._bias):
+            first = self._bias_times(t0)
+            if first:
+                probe[first[0]] = rhs.bias_at(first[0])
+        spatial = any(np.shape(v) != (3,) for v in probe.values())
         n_bias = max(len(self._bias_times(t0)), 1)
+
+        def bias_at(tt):
+            return probe.pop(tt) if tt in probe else rhs.bias_at(tt)
+
         field_chunk = max(1, self.STAGE_FIELD_BYTES // (n_bias * 24 * grid.n_cells))
         while k < n_total:
             to_sample = self.sample_every - (k % self.sample_every)
@@ -515,7 +527,7 @@ class Simulation:
                 i = 0
                 for s in range(chunk):
                     for tt in self._bias_times(t0 + (k + s) * sp.dt):
-                        v = rhs.bias_at(tt)
+                        v = bias_at(tt)
                         flds[i] = v[:, None, None, None] if v.shape == (3,) else v
                         i += 1
                 args.stage_bias_fields = L.dptr(flds)
@@ -525,7 +537,7 @@ class Simulation:
                 rows = []
                 for s in range(chunk):
                     for tt in self._bias_times(t0 + (k + s) * sp.dt):
-                        v = rhs.bias_at(tt)
+                        v = bias_at(tt)
                         if v.shape != (3,):
                             raise ValueError("a bias callable must return the same shape at every t")
                         rows.append(v)
@@ -553,6 +565,9 @@ class Simulation:
             if rc == L.EDEAD:
                 pull()
                 _raise_dead(grid, int(stats.dead_flat))
+            if rc != L.OK:
+                # keep SimState consistent (t/step were advanced by steps_done)
+                pull()
             L.check(rc, "run")
             traj.final_residual = float(stats.residual)
             equilibrated = stats.status == L.EQUILIBRATED

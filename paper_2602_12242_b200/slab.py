@@ -174,6 +174,7 @@ class CudaSlabBackend:
         self.halo = {k: torch.zeros(hshape, dtype=torch.float64, device=self.dev)
                      for k in ("send_lo", "send_hi", "lo", "hi")}
         self.red = torch.zeros(8, dtype=torch.float64, device=self.dev)
+        self.mhalo = None   # neighbour planes of (Ms, A): set by material_halos
         if self.d is not None:
             L.check(lib.mxb_demag_set_stream(self.d, C.c_void_p(self.stream)))
             s, r = C.c_void_p(), C.c_void_p()
@@ -195,6 +196,34 @@ class CudaSlabBackend:
         self.halo["send_hi"].copy_(f[:, -1])
         return self.halo["send_lo"], self.halo["send_hi"], self.halo["lo"], self.halo["hi"]
 
+    def material_halos(self, comm, lo_rank, hi_rank):
+        """Swap the boundary planes of Ms and A with the z-neighbours once, so
+        the stage kernel sees the neighbours' material across the slab faces
+        (validity and the harmonic exchange coefficient, fields.py:59-92)."""
+        if lo_rank is None and hi_rank is None:
+            return
+        mat, p = self.mat, self.plan
+        shape = (p.nz_local, p.ny, p.nx)
+        Ms = np.broadcast_to(mat.Ms, shape)
+        A = np.broadcast_to(mat.A, shape)
+        send_lo = self.new_tensor(np.stack([Ms[0], A[0]]))
+        send_hi = self.new_tensor(np.stack([Ms[-1], A[-1]]))
+        recv_lo = self.torch.zeros_like(send_lo)
+        recv_hi = self.torch.zeros_like(send_hi)
+        comm.halos(send_lo, send_hi, recv_lo, recv_hi, lo_rank, hi_rank)
+        if mat._Ms_u is not None and mat._A_u is not None:
+            # uniform local material: the uniform kernels take the neighbours'
+            # material to be the local one -- check that it is
+            for r, rk in ((recv_lo, lo_rank), (recv_hi, hi_rank)):
+                if rk is None:
+                    continue
+                h = r.cpu().numpy()
+                if np.any(h[0] != mat._Ms_u) or np.any(h[1] != mat._A_u):
+                    raise ValueError("the material changes across a slab boundary but is uniform on this "
+                                     "rank; pass it per cell (a non-uniform MaterialMap) on every rank")
+            return
+        self.mhalo = (recv_lo, recv_hi)
+
     # -- demag ----------------------------------------------------------------------
     def demag_x_forward(self, src):
         L.check(L.load().mxb_demag_x_forward(self.d, C.c_void_p(self.fields[src].data_ptr())))
@@ -215,6 +244,13 @@ class CudaSlabBackend:
         io.hd, io.k1, io.s, io.k1_out = ptr(hd), ptr(k1), ptr(s), ptr(k1_out)
         io.halo_lo = C.c_void_p(self.halo["lo"].data_ptr()) if halo_lo else None
         io.halo_hi = C.c_void_p(self.halo["hi"].data_ptr()) if halo_hi else None
+        if self.mhalo is not None:
+            lo, hi = self.mhalo
+            plane = lo.shape[1] * lo.shape[2] * 8
+            if halo_lo:
+                io.hms_lo, io.hA_lo = C.c_void_p(lo.data_ptr()), C.c_void_p(lo.data_ptr() + plane)
+            if halo_hi:
+                io.hms_hi, io.hA_hi = C.c_void_p(hi.data_ptr()), C.c_void_p(hi.data_ptr() + plane)
         io.bias = (C.c_double * 3)(*bias)
         io.c, io.dt6, io.renorm = c, dt6, 1 if renorm else 0
         L.check(self.ctx.call("mxb_stage_dev", mode, C.byref(terms), C.byref(io)), "stage")
@@ -259,7 +295,8 @@ class SlabSimulation:
     """Fixed-step RK4/Euler loop on a z-slab (the multi-rank Simulation.run_until core)."""
 
     def __init__(self, plan: SlabPlan, backend, comm: Comm, terms: L.Terms, *, method="rk4",
-                 dt: float, bias=None, periodic_z=False, use_demag=True, renorm_each_stage=True):
+                 dt: float, bias=None, periodic_z=False, use_demag=True, renorm_each_stage=True,
+                 check_every: int = 16):
         if method not in ("rk4", "euler"):
             raise ValueError(f"unknown method {method!r}")
         self.plan, self.b, self.comm, self.terms = plan, backend, comm, terms
@@ -271,6 +308,10 @@ class SlabSimulation:
         self.cur = "Y0"
         self.t0 = 0.0
         self.step = 0
+        # the step commit runs on the device (every rank applies the same
+        # all-reduced totals; after a halt the stage kernels are no-ops), so the
+        # host reads the control block only every check_every steps
+        self.check_every = max(1, int(check_every))
 
     def _bias_at(self, t):
         if self.bias is None:
@@ -307,6 +348,8 @@ class SlabSimulation:
         self.n_magnetic = int(round(tot[3]))
         self.mean0 = tot[:3] / self.n_magnetic
         b.ctl_reset(self.mean0, self.n_magnetic, -1.0 if eq_tol is None else eq_tol)
+        if hasattr(b, "material_halos"):
+            b.material_halos(self.comm, self.lo_rank, self.hi_rank)
 
     def run(self, nsteps: int):
         """Advance up to nsteps; stops early on blow-up, a dead cell or equilibrium.
@@ -318,7 +361,10 @@ class SlabSimulation:
         else:
             stages, offs = RK4_STAGES, (0.0, 0.5 * dt, 0.5 * dt, dt)
         st = b.ctl_get()
-        for _ in range(nsteps):
+        done0 = int(st.steps_done)
+        cur0, step0 = self.cur, self.step
+        for i in range(nsteps):
+            # issued as if every step commits; corrected from steps_done at each check
             y, yn = self.cur, nxt[self.cur]
             tb = self.t0 + self.step * dt
             for (mode, ys, out, c), off in zip(stages, offs):
@@ -332,18 +378,20 @@ class SlabSimulation:
                         bias=self._bias_at(tb if off == 0.0 else tb + off),
                         c=(c or 0.0) * dt, dt6=dt / 6.0,
                         renorm=self.renorm if mode in (2, 3, 4) else True)
-            before = int(st.steps_done)
             p = b.partials()
             s, mx = p[:4].clone(), p[4:].clone()
             self.comm.allreduce(s, "sum")
             self.comm.allreduce(mx, "max")
             b.commit(b.torch.cat([s, mx]))
-            st = b.ctl_get()
-            if st.steps_done > before:
-                self.cur = yn
-                self.step += 1
-            if st.status != 0:
-                break
+            self.cur = yn
+            self.step += 1
+            if (i + 1) % self.check_every == 0 or i + 1 == nsteps:
+                st = b.ctl_get()
+                done = int(st.steps_done) - done0
+                self.step = step0 + done
+                self.cur = cur0 if done % 2 == 0 else nxt[cur0]
+                if st.status != 0:
+                    break
         return st
 
     def state(self):

@@ -48,8 +48,10 @@ class NumpySlabBackend:
 
     def _slice_mat(self, za, zb):
         m = self.matg
+        sl = (lambda a: None if a is None else a[za:zb])  # noqa: E731
         return O.Mat((m.dims[0], m.dims[1], zb - za), m.cell, m.Ms[za:zb], m.A[za:zb], m.Ku[za:zb],
-                     m.D[za:zb], m.alpha[za:zb], m.eK[:, za:zb], m.gamma)
+                     m.D[za:zb], m.alpha[za:zb], m.eK[:, za:zb], m.gamma, sl(m.Kc1), m.c1, m.c2,
+                     sl(m.Db))
 
     # -- data movement -----------------------------------------------------------
     def upload(self, name, host):
@@ -111,6 +113,8 @@ class NumpySlabBackend:
     def stage(self, mode, terms: L.Terms, *, ys, y, out, hd=None, k1=None, s=None, k1_out=None,
               halo_lo=False, halo_hi=False, bias=(0.0, 0.0, 0.0), c=0.0, dt6=0.0, renorm=True):
         p = self.plan
+        if self.ctl.status:
+            return   # halted: the device stage kernels are no-ops too
         f = {k: v.numpy() for k, v in self.fields.items()}
         m = f[ys]
         parts = ([self.halo["lo"].numpy()[:, None]] if halo_lo else []) + [m] + \
@@ -121,7 +125,8 @@ class NumpySlabBackend:
         mask = terms.mask
         ghost = {0: "neumann", 1: "dmi", 2: "periodic"}[terms.ghost_mode]
         tl = O.Terms(exchange=bool(mask & L.TERM_EXCHANGE), anisotropy=bool(mask & L.TERM_ANISOTROPY),
-                     dmi=bool(mask & L.TERM_DMI), ghost_mode=ghost)
+                     dmi=bool(mask & L.TERM_DMI), ghost_mode=ghost, cubic=bool(mask & L.TERM_CUBIC),
+                     bulk_dmi=bool(mask & L.TERM_BULK_DMI))
         h = O.h_eff(0.0, ext, matx, tl)
         lo = 1 if halo_lo else 0
         h = h[:, lo:lo + p.nz_local]

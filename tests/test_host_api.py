@@ -151,10 +151,38 @@ def test_prefault_buffer_is_zeroed_fresh_array():
         assert not np.any(buf)
 
 
-def test_prefault_threads_keep_the_buffer_alive():
+def test_prefault_threads_keep_the_buffer_alive(monkeypatch):
+    """An abandoned run drops its reference to the prefault buffer at once; the
+    fill threads must keep the array alive until their memset is done."""
     import gc
-    from paper_2602_12242_b200.llg import _prefault
-    _, threads = _prefault((3, 64, 64, 64), nthreads=4)   # buffer dropped at once
+    import threading
+    import weakref
+
+    from paper_2602_12242_b200 import llg
+    go = threading.Event()
+    seen = []
+    real = llg._zero_range
+
+    def gated(buf, offset, nbytes):
+        go.wait(10)
+        real(buf, offset, nbytes)
+        seen.append(bool(np.all(buf.reshape(-1).view(np.uint8)[offset:offset + nbytes] == 0)))
+
+    monkeypatch.setattr(llg, "_zero_range", gated)
+    buf, threads = llg._prefault((3, 64, 64, 64), nthreads=4)
+    buf[...] = 1.0
+    wr = weakref.ref(buf)
+    del buf
     gc.collect()
+    assert wr() is not None        # held by the waiting fill threads
+    go.set()
     for th in threads:
         th.join()
+    assert seen == [True] * len(threads)
+
+
+def test_direct_sum_guard():
+    """reference tests/test_demag.py:82-86 (raised before any device work)"""
+    g = mx.GridSpec(17, 17, 17, 1e-9, 1e-9, 1e-9)
+    with pytest.raises(ValueError, match="direct sum limited"):
+        mx.demag_field_direct(mx.VectorField3(g, np.zeros((3,) + g.shape)), g)

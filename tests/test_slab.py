@@ -31,38 +31,59 @@ def free_port():
     return p
 
 
-def problem():
-    mat = O.make_mat((NX, NY, NZ), CELL, 8e5, A=1.3e-11, Ku=5e4, eK=(0.3, 0.2, 1.0), D=1e-3,
-                     alpha=0.1)
+def _disk_ms():
+    y, x = np.mgrid[0:NY, 0:NX]
+    inside = ((x - (NX - 1) / 2) / (NX / 2)) ** 2 + ((y - (NY - 1) / 2) / (NY / 2)) ** 2 <= 1.0
+    return np.broadcast_to(np.where(inside, 8e5, 0.0), (NZ, NY, NX)).copy()
+
+
+def _mat_kw(case):
+    """uniform: the round-1 problem; disk: per-cell Ms (vacuum outside an
+    elliptic disk), A varying along z (so the slab faces see a different
+    neighbour A), plus cubic anisotropy and bulk DMI."""
+    kw = dict(A=1.3e-11, Ku=5e4, eK=(0.3, 0.2, 1.0), D=1e-3, alpha=0.1)
+    if case == "disk":
+        kw["A"] = 1.3e-11 * (1.0 + 0.1 * np.arange(NZ))[:, None, None] * np.ones((NZ, NY, NX))
+        kw.update(Kc1=3e4, c1=(1.0, 1.0, 0.0), c2=(-1.0, 1.0, 0.5), Db=1.2e-3)
+        return _disk_ms(), kw
+    return 8e5, kw
+
+
+def problem(case="uniform"):
+    ms, kw = _mat_kw(case)
+    mat = O.make_mat((NX, NY, NZ), CELL, ms, **kw)
     rng = np.random.default_rng(21)
     m0 = O.renormalize(rng.normal(size=(3, NZ, NY, NX)), mat)
     packed = O.packed_tensor(NX, NY, NZ, *CELL)
     return mat, m0, packed
 
 
-def reference():
-    mat, m0, packed = problem()
+def reference(case="uniform"):
+    mat, m0, packed = problem(case)
+    extra = case == "disk"
     terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=O.kernel_spectra(packed),
-                    bias=np.array(BIAS))
+                    bias=np.array(BIAS), cubic=extra, bulk_dmi=extra)
     return O.run(m0, mat, terms, "rk4", DT, max_steps=NSTEPS, sample_every=1)
 
 
-def _terms():
+def _terms(case="uniform"):
     from paper_2602_12242_b200 import _lib as L
-    return L.Terms(L.TERM_EXCHANGE | L.TERM_ANISOTROPY | L.TERM_DMI | L.TERM_DEMAG | L.TERM_BIAS,
-                   L.GHOST["dmi"], 1, 1)
+    mask = L.TERM_EXCHANGE | L.TERM_ANISOTROPY | L.TERM_DMI | L.TERM_DEMAG | L.TERM_BIAS
+    if case == "disk":
+        mask |= L.TERM_CUBIC | L.TERM_BULK_DMI
+    return L.Terms(mask, L.GHOST["dmi"], 1, 1)
 
 
-def _worker(rank, world, port, kind, out):
+def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2602_12242_b200.slab import Comm, SlabPlan, SlabSimulation
-    mat, m0, packed = problem()
+    mat, m0, packed = problem(case)
     plan = SlabPlan(NX, NY, NZ, world, rank)
     z0, nzl = plan.z0, plan.nz_local
-    terms = _terms()
+    terms = _terms(case)
     if kind == "numpy":
         from tests.slab_numpy import NumpySlabBackend
         b = NumpySlabBackend(plan, mat, O.kernel_spectra(packed), terms)
@@ -74,24 +95,27 @@ def _worker(rank, world, port, kind, out):
         from paper_2602_12242_b200.slab import CudaSlabBackend
         torch.cuda.set_device(0)
         gl = mx.GridSpec(NX, NY, nzl, *CELL)
-        mat_l = mx.MaterialMap(gl, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.3, 0.2, 1.0), D=1e-3, alpha=0.1)
+        ms, kw = _mat_kw(case)
+        sl = (lambda a: a[z0:z0 + nzl] if np.ndim(a) == 3 else a)  # noqa: E731
+        kw = {k: sl(v) for k, v in kw.items()}
+        mat_l = mx.MaterialMap(gl, Ms=sl(ms), **kw)
         h = C.c_void_p()
         L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(NX, NY, NZ, *CELL)._c()), 0, world,
                                                rank, C.byref(h)))
         L.check(L.load().mxb_demag_set_packed(h, L.dptr(np.ascontiguousarray(packed))))
         b = CudaSlabBackend(plan, gl, mat_l, h, 0)
-    sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=DT, bias=BIAS)
+    sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=DT, bias=BIAS, check_every=check_every)
     sim.start(m0[:, z0:z0 + nzl])
     st = sim.run(NSTEPS)
     out[rank] = (sim.state(), st.steps_done, np.array(st.mean[:3]), st.status)
     dist.destroy_process_group()
 
 
-def _run(kind):
+def _run(kind, case="uniform", check_every=16):
     world = 2
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, free_port(), kind, out), nprocs=world,
+    mp.start_processes(_worker, args=(world, free_port(), kind, out, case, check_every), nprocs=world,
                        start_method="spawn", join=True)
     state = np.concatenate([out[r][0] for r in range(world)], axis=1)
     return state, out[0][1], out[0][2], out[0][3], out[1][2]
@@ -110,9 +134,10 @@ def test_slab_plan_chunks_cover_the_spectrum():
         SlabPlan(8, 8, 6, 4, 0)
 
 
-def test_slab_numpy_gloo_matches_single_domain():
-    ref = reference()
-    state, steps, mean0, status, mean1 = _run("numpy")
+@pytest.mark.parametrize("case,check_every", [("uniform", 16), ("uniform", 1), ("disk", 2)])
+def test_slab_numpy_gloo_matches_single_domain(case, check_every):
+    ref = reference(case)
+    state, steps, mean0, status, mean1 = _run("numpy", case, check_every)
     assert steps == NSTEPS and status == 0
     assert np.max(np.abs(state - ref.m)) <= 1e-12 * 8e5
     assert np.array_equal(mean0, mean1)              # every rank committed the same step
@@ -120,9 +145,12 @@ def test_slab_numpy_gloo_matches_single_domain():
 
 
 @pytest.mark.gpu
-def test_slab_cuda_two_ranks_match_single_domain():
-    ref = reference()
-    state, steps, mean0, status, mean1 = _run("cuda")
+@pytest.mark.parametrize("case", ["uniform", "disk"])
+def test_slab_cuda_two_ranks_match_single_domain(case):
+    """disk: per-cell Ms and A across the slab faces (the neighbours' material
+    planes are swapped once at start), cubic anisotropy and bulk DMI."""
+    ref = reference(case)
+    state, steps, mean0, status, mean1 = _run("cuda", case)
     assert steps == NSTEPS and status == 0
     assert np.max(np.abs(state - ref.m)) <= 1e-11 * 8e5
     assert np.array_equal(mean0, mean1)
