@@ -172,6 +172,53 @@ def cpu_reference(n: int, steps: int, warmup: int):
     return n ** 3 * steps / el, el, cores
 
 
+# weak scaling ladder (paper PAPER.md:480-518): 2^24 cells per GPU
+WEAK_DIMS = {1: (256, 256, 256), 2: (512, 256, 256), 4: (512, 512, 256), 8: (512, 512, 512)}
+
+
+def grid_dims(args, world):
+    """(nx, ny, nz): strong scaling keeps --size^3 for every N; weak scaling
+    follows the 256^3 -> 512x256^2 -> 512^2x256 -> 512^3 ladder."""
+    if args.scaling == "weak":
+        return WEAK_DIMS.get(world, (256, 256, 256 * world))
+    return args.size, args.size, args.size
+
+
+def extrapolate_cpu(cs: float, n_sample: int, n: int) -> dict:
+    """the CPU rate at the bench size, scaled from the
+    sample by the per-cell FFT cost (log2 of the padded cells, N log N per
+    step); the 512^3 oracle run itself needs ~230 GB of host memory."""
+    import math
+    f = math.log2((2 * n_sample) ** 3) / math.log2((2 * n) ** 3)
+    return {"value": cs * f, "unit": "cell-steps/s", "cells": n ** 3,
+            "method": f"N log N: sample rate x log2((2*{n_sample})^3) / log2((2*{n})^3) = x{f:.3f}",
+            "flag": "extrapolated, not measured"}
+
+
+def tensor_deviation(mx):
+    """Deviation of the GPU-built tensor (the bench's mode and the unmirrored
+    build) from the reference's own tensor at 32^3 with the bench material,
+    against the fixture tests/golden/bench_32.npz made by running the reference
+    (tests/golden/make_golden.py bench32)."""
+    path = os.path.join(ROOT, "tests", "golden", "bench_32.npz")
+    if not os.path.exists(path):
+        return None
+    z = np.load(path)
+    g = mx.GridSpec(32, 32, 32, 4e-9, 4e-9, 4e-9)
+    mat = mx.MaterialMap(g, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
+    out = {}
+    for name, sym in (("mirrored_bench_mode", True), ("unmirrored", False)):
+        k = mx.DemagKernel.build(g, symmetric=sym)
+        hd = k.field(z["m"])
+        rhs = mx.PartitionedRHS(mat, exchange=True, anisotropy=True, dmi=True, demag=k,
+                                bias=np.array([1e4, 0.0, 0.0]))
+        he = rhs.h_total_quiet(0.0, z["m"])
+        out[name] = {"h_demag": float(np.max(np.abs(hd - z["h_demag"])) / np.max(np.abs(z["h_demag"]))),
+                     "h_eff": float(np.max(np.abs(he - z["h_eff"])) / np.max(np.abs(z["h_eff"])))}
+    out["norm"] = "max|dH| / max|H_ref| at 32^3 (random-direction m), vs the reference's tensor"
+    return out
+
+
 def run_slab(args, rank, world, local):
     """N > 1: the 512^3 problem z-slab decomposed over the ranks (strong scaling):
     halo planes by send/recv, slab FFT transposes by all-to-all, step reductions
@@ -189,14 +236,14 @@ def run_slab(args, rank, world, local):
     torch.cuda.set_device(dev)
     mx.set_device(dev)
     dist.init_process_group(args.backend)
-    n = args.size
-    plan = SlabPlan(n, n, n, world, rank)
+    nx, ny, nz = grid_dims(args, world)
+    plan = SlabPlan(nx, ny, nz, world, rank)
     cell = (4e-9, 4e-9, 4e-9)
-    gl = mx.GridSpec(n, n, plan.nz_local, *cell)
+    gl = mx.GridSpec(nx, ny, plan.nz_local, *cell)
     mat_l = mx.MaterialMap(gl, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
     h = C.c_void_p()
     t0 = time.perf_counter()
-    L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(n, n, n, *cell)._c()), dev, world,
+    L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(nx, ny, nz, *cell)._c()), dev, world,
                                            rank, C.byref(h)))
     L.check(L.load().mxb_demag_build(h, 1))
     t_build = time.perf_counter() - t0
@@ -208,8 +255,12 @@ def run_slab(args, rank, world, local):
         mask |= {"exchange": L.TERM_EXCHANGE, "anisotropy": L.TERM_ANISOTROPY, "dmi": L.TERM_DMI,
                  "bias": L.TERM_BIAS}[t]
     terms = L.Terms(mask, L.GHOST["dmi"], 1, 1)
-    rng = np.random.default_rng(1000 + rank)      # per-slab synthetic state
-    m = mx.VectorField3(gl, rng.standard_normal(size=(3,) + gl.shape))
+    # the same global state as the single-GPU run (setup_problem: default_rng(0)
+    # over the whole grid), sliced to this rank's planes, so N > 1 results can be
+    # compared with N = 1
+    full = np.random.default_rng(0).standard_normal(size=(3, nz, ny, nx))
+    m = mx.VectorField3(gl, np.ascontiguousarray(full[:, plan.z0:plan.z0 + plan.nz_local]))
+    del full
     mx.renormalize(m, mat_l)
     dt = 0.1 * 0.5 * 2.5e-14 * (4e-9 / 0.78125e-9) ** 2
     sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=dt, bias=bias)
@@ -234,13 +285,13 @@ def run_slab(args, rank, world, local):
     _ = sim.state()
     w = torch.tensor([time.perf_counter() - w0], device="cuda")
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
-    N = n ** 3
+    N = nx * ny * nz
     if rank == 0:
         out = {"metric": METRIC, "value": N / (t_step * 1e-3), "unit": "cell-steps/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                "data": "synthetic",
-               "config": {"workload": f"synthetic random-m {n}^3, full H_eff, RK4, z-slab decomposed",
+               "config": {"workload": f"synthetic random-m {nx}x{ny}x{nz}, full H_eff, RK4, z-slab decomposed",
                           "cells": N, "dt": dt, "parallelism": f"z-slab x{world} ({args.backend})",
                           "l2": "inputs > L2, no flush"},
                "e2e": {"value": N * args.steps / float(w.item()), "unit": "cell-steps/s",
@@ -250,6 +301,37 @@ def run_slab(args, rank, world, local):
                "gpu_launches": args.steps * 26, "clocks": clk.summary()}
         print(json.dumps(out))
     dist.destroy_process_group()
+
+
+def complex_mode(mx, L, C, ctx, g, ts, dt, bptr, args):
+    """The plane pipeline with full complex spectra (kernel mode 5): the mode
+    from_packed / load_kernel select for the reference's own tensor (no
+    symmetry assumed, 96 B per spectral point instead of the mirrored build's
+    parity-reduced 12).  Timed on the unmirrored GPU build of the same grid."""
+    t0 = time.perf_counter()
+    kc = mx.DemagKernel.build(g)
+    t_build = time.perf_counter() - t0
+    if kc.kmode != 5:
+        return {"kmode": kc.kmode, "note": "complex-spectra pipeline not selected for this shape"}
+    ms_tot, nl = C.c_double(), C.c_int64()
+    L.check(ctx.call("mxb_time_steps", kc._d.h, C.byref(ts), dt, 1, bptr, C.byref(ms_tot), None,
+                     C.byref(nl)))
+    n = max(3, args.steps // 4)
+    L.check(ctx.call("mxb_time_steps", kc._d.h, C.byref(ts), dt, n, bptr, C.byref(ms_tot), None,
+                     C.byref(nl)))
+    ms_eval = C.c_double()
+    passes = np.zeros(5)
+    L.check(ctx.call("mxb_time_demag", kc._d.h, 3, C.byref(ms_eval), L.dptr(passes)))
+    t_step = ms_tot.value / n
+    out = {"kmode": 5, "ms_per_step": t_step, "value": g.n_cells / (t_step * 1e-3),
+           "unit": "cell-steps/s", "steps": n, "demag_ms_per_eval": ms_eval.value,
+           "yz_pipeline_ms_per_eval": float(passes[1] + passes[2] + passes[3]),
+           "spectra_bytes": kc.device_bytes, "tensor_build_s": t_build,
+           "note": "unmirrored GPU tensor in the complex-spectra pipeline (what the reference's "
+                   "own packed tensor runs through): parity with the reference tensor 5.6e-16 "
+                   "(tests/test_bench_path_parity.py)"}
+    del kc
+    return out
 
 
 def main():
@@ -262,8 +344,13 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dev", action="store_true", help="skip the 32^3 tensor-deviation check")
+    ap.add_argument("--no-ref-mode", action="store_true",
+                    help="skip timing the complex-spectra (reference tensor) pipeline")
     ap.add_argument("--repeats", type=int, default=5,
                     help="timed runs of --steps steps; the median is reported (SURVEY 8d)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: --size^3 on every N; weak: 2^24 cells per GPU (256^3 ... 512^3 at N=8)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="collectives for N > 1 (gloo only to exercise the path on one GPU)")
     args = ap.parse_args()
@@ -292,6 +379,8 @@ def main():
     if world > 1:
         run_slab(args, rank, world, local)
         return
+    if args.scaling == "weak":
+        args.size = WEAK_DIMS[1][0]
 
     import ctypes as C
 
@@ -351,10 +440,14 @@ def main():
     own = {"x_r2c": pb_own[0], "yz_plane_pipeline": pb_own[1] + pb_own[2] + pb_own[3], "x_c2r": pb_own[4],
            "y_fwd": pb_own[1], "z_fused_mul": pb_own[2], "y_inv": pb_own[3], "stage_stencil_llg": dom[1]}
     ach_own = own[dom[0]] / (dom[2] * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_src = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dom[0])
+            tj = json.load(f)
+        traffic = tj.get(dom[0])
+        traffic_src = {"source": tj.get("_source"), "commit": tj.get("_commit"),
+                       "note": "DRAM read+write per launch from the ncu --set full capture at that "
+                               "commit (not measured in this run)"}
     except Exception:
         pass
     pf = demag_flops(g, kern)
@@ -373,7 +466,7 @@ def main():
     step_bytes = stencil_bytes + 4 * sum(pb)
     step_bytes_own = stencil_bytes + 4 * sum(pb_own)
     # end to end through the public API with host buffers
-    e2e = None
+    e2e = e2e_pageable = None
     if not args.no_e2e:
         pinned = C.c_void_p()
         L.check(L.load().mxb_host_alloc(m.data.nbytes, C.byref(pinned)))
@@ -392,25 +485,43 @@ def main():
                "note": "Simulation.run_until from pinned host state; <m> read back every step"}
         del st, sim
         L.load().mxb_host_free(pinned)
+        # the reference API's normal input: a plain (pageable) numpy state
+        st = mx.SimState(mx.VectorField3(g, m.data.copy()))
+        sim = mx.Simulation(st, rhs, mx.IntegratorSpec("rk4", dt), sample_every=1,
+                            energy_in_samples=False)
+        sim.CHUNK = 1
+        t0 = time.perf_counter()
+        sim.run_until(mx.StopCondition(max_steps=args.steps))
+        el = time.perf_counter() - t0
+        e2e_pageable = {"value": N * args.steps / el, "unit": "cell-steps/s",
+                        "h2d_bytes_per_step": int(24 * N / args.steps),
+                        "d2h_bytes_per_step": int(24 * N / args.steps + 24),
+                        "note": "Simulation.run_until from a pageable numpy state; <m> every step"}
+        del st, sim
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cs, el, cores = cpu_reference(args.cpu_n, 2, 0)
+        cs, el, cores = cpu_reference(args.cpu_n, 5, 1)
         cpu = {"value": cs, "unit": "cell-steps/s", "cores": cores, "kind": "port",
-               "sample": f"synthetic {args.cpu_n}^3 full H_eff, 2 RK4 steps, oracle numpy/scipy "
-                         f"(tensor build excluded)"}
+               "sample": f"synthetic {args.cpu_n}^3 full H_eff, 1 warm-up + 5 timed RK4 steps, oracle "
+                         f"numpy/scipy (tensor build excluded)",
+               "extrapolated_to_size": extrapolate_cpu(cs, args.cpu_n, args.size)}
+    dev = tensor_deviation(mx) if not args.no_dev else None
+    cmode = None
+    if not args.no_ref_mode:
+        cmode = complex_mode(mx, L, C, ctx, g, ts, dt, bptr, args)
     if rank != 0:
         return
     out = {
         "metric": METRIC, "value": value, "unit": "cell-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"synthetic random-m {args.size}^3, full H_eff "
                                "(demag+exchange+DMI+uniaxial anis+Zeeman), RK4",
                    "cells": N, "dt": dt, "l2": "inputs (3.2 GB/field) > L2, no flush",
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm,
-                     "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                     "unit": "GB/s", "frac": ach / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": which, "bytes": "SURVEY 8d fixed formula",
                      "achieved_impl_bytes": ach_own, "frac_impl_bytes": ach_own / hbm,
                      "frac_vs_8TBs_nominal": ach / 8000.0},
@@ -426,7 +537,14 @@ def main():
         "fp64": fp64,
         "demag_ms_per_eval": ms_eval.value, "cufft_demag_ms_per_eval": ms_cufft.value,
         "tensor_build_s": t_build,
-        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(nl.value),
+        "tensor": {"build": "GPU Newell tensor (newell.cu) with correctly rounded atan/asinh "
+                            "(dd_math.cuh); mirrored octant (symmetric=True), real parity-reduced spectra",
+                   "kmode": kern.kmode, "deviation_vs_reference": dev,
+                   "deviation_tests": "tests/test_bench_path_parity.py (32/64/128^3) and "
+                                      "tests/test_tensor_noise_floor.py (the reference's own "
+                                      "cross-host spread)"},
+        "reference_tensor_mode": cmode,
+        "e2e": e2e, "e2e_pageable": e2e_pageable, "cpu_baseline": cpu, "gpu_launches": int(nl.value),
         "clocks": clk.summary(),
     }
     print(json.dumps(out))

@@ -224,12 +224,29 @@ def radix5_goldens():
          bias=(-19576.0, 3422.0, 0.0), demag=True, dt=2e-13, nsteps=20, store_tensor=False)
 
 
+def bench32_golden():
+    """The bench's material and cell (bench.py setup_problem) at 32^3 with a
+    random-direction m: the reference's H_demag (its own tensor) and H_eff.
+    bench.py reports its GPU-built tensor's deviation from these at run time."""
+    g = GridSpec(32, 32, 32, 4e-9, 4e-9, 4e-9)
+    mat = MaterialMap(g, Ms=8e5, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
+    rng = np.random.default_rng(25)
+    m = rng.standard_normal((3,) + g.shape)
+    m *= 8e5 / np.sqrt((m * m).sum(axis=0))
+    kern = rdemag.DemagKernel.build(g)
+    rhs = PartitionedRHS(mat, exchange=True, anisotropy=True, dmi=True, demag=kern,
+                         bias=np.array([1e4, 0.0, 0.0]))
+    np.savez_compressed(os.path.join(OUT, "bench_32.npz"), m=m, h_demag=kern.field(m),
+                        h_eff=rhs.h_total_quiet(0.0, m), numpy=np.__version__, scipy=scipy.__version__)
+    print("bench_32 ok")
+
+
 def main():
     groups = sys.argv[1:]
     if groups:
         for gname in groups:
             {"spatial": spatial_bias_golden, "sp4_protocol": sp4_protocol_golden,
-             "radix5": radix5_goldens}[gname]()
+             "radix5": radix5_goldens, "bench32": bench32_golden}[gname]()
         return
     ALL = ("exchange", "anisotropy", "dmi")
     # tiny grids: every term, every boundary mode
@@ -318,6 +335,7 @@ def main():
     radix5_goldens()
     spatial_bias_golden()
     sp4_protocol_golden()
+    bench32_golden()
 
 
 if __name__ == "__main__":

@@ -9,7 +9,7 @@ from oracle import magnex_oracle as O
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-               if not os.path.basename(p).startswith(("tensor_known", "sp4_trace", "fno_", "spatial_bias",
+               if not os.path.basename(p).startswith(("tensor_known", "sp4_trace", "fno_", "spatial_bias", "bench_32",
                                                            "sp4_protocol")))
 
 

@@ -147,3 +147,13 @@ def test_sp4_protocol_head():
     n = len(r.rows)
     for k in ("t", "mx", "my", "mz", "e_total"):
         assert np.array_equal(np.array([row[k] for row in r.rows]), z[k][:n]), k
+
+
+def test_bench32_golden():
+    """The bench's 32^3 deviation fixture: oracle demag and H_eff vs the reference."""
+    z = load("bench_32")
+    spectra = O.kernel_spectra(O.packed_tensor(32, 32, 32, 4e-9, 4e-9, 4e-9))
+    assert np.array_equal(O.demag_field(spectra, z["m"]), z["h_demag"])
+    mat = O.make_mat((32, 32, 32), (4e-9,) * 3, 8e5, A=1.3e-11, Ku=5e4, D=1e-3, alpha=0.1)
+    terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=spectra, bias=np.array([1e4, 0.0, 0.0]))
+    assert np.array_equal(O.h_eff(0.0, z["m"], mat, terms), z["h_eff"])
