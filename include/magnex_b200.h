@@ -226,6 +226,9 @@ int mxb_demag_create_slab(const mxb_grid* global_grid, int device, int nranks, i
  * block_elems = complex elements per all-to-all block */
 int mxb_demag_slab_info(mxb_demag* d, int64_t info[8]);
 int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv);
+/* complex elements per all-to-all block of the slab buffers (depends on the
+ * spectra layout chosen by set_packed / build: call after them) */
+int mxb_demag_slab_block(mxb_demag* d, int64_t* elems);
 int mxb_demag_x_forward(mxb_demag* d, const double* m_dev);
 int mxb_demag_yz(mxb_demag* d);
 int mxb_demag_x_inverse(mxb_demag* d, double* h_dev);

@@ -104,6 +104,7 @@ SIGNATURES = {
     "mxb_demag_create_slab": ([C.POINTER(Grid), C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "mxb_demag_slab_info": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "mxb_demag_slab_buffers": ([C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
+    "mxb_demag_slab_block": ([C.c_void_p, C.POINTER(C.c_int64)], C.c_int),
     "mxb_demag_x_forward": ([C.c_void_p, C.c_void_p], C.c_int),
     "mxb_demag_yz": ([C.c_void_p], C.c_int),
     "mxb_demag_x_inverse": ([C.c_void_p, C.c_void_p], C.c_int),

@@ -272,6 +272,12 @@ int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv) {
     return MXB_OK;
 }
 
+int mxb_demag_slab_block(mxb_demag* d, int64_t* elems) {
+    if (!d || !elems) { set_error("null argument"); return MXB_EINVAL; }
+    *elems = d->plan.blk;
+    return MXB_OK;
+}
+
 int mxb_demag_x_forward(mxb_demag* d, const double* m) {
     if (!d || !m) { set_error("null argument"); return MXB_EINVAL; }
     cudaSetDevice(d->plan.dev);

@@ -333,6 +333,7 @@ int DemagPlan::init(const mxb_grid& gr, int device, int nranks, int rk) {
     kx0 = rank * CH;
     kxn = std::max(0, std::min(CH, hx - kx0));
     blk = (long long)nz_l * g.ny * CHP * 3;
+    xblk = blk;
     MXB_CUDA(cudaSetDevice(dev));
     int rc = set_smem_attrs();
     if (rc) return rc;
@@ -362,7 +363,10 @@ int DemagPlan::init(const mxb_grid& gr, int device, int nranks, int rk) {
 // shapes the plane pipeline covers (single rank, 3-D, ny == nz, power-of-two
 // padding, fast x rows); MXB_PIPE=0 disables it, MXB_PIPE=1 lifts the size floor
 bool DemagPlan::pipe_candidate(bool symmetric) const {
-    if (G != 1 || pz <= 1 || py <= 1 || !fast) return false;
+    if (pz <= 1 || py <= 1 || !fast) return false;
+    // z slab: the pipeline runs on the rank's kx chunk of all nz planes, read in
+    // place from the all-to-all receive blocks (pairs of rows need even nz_l)
+    if (G > 1 && (nz_l % 2)) return false;
     if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
     if (!pipe_shape_ok(g.ny, g.nz)) return false;
     if (!symmetric && !pipe_cplx_ok(pz)) return false;
@@ -497,23 +501,34 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         CHP = hxp;
         blk = (long long)nz_l * g.ny * CHP * 3;
     }
+    xblk = blk;
     if (pipe_candidate(symmetric)) {
         // plane-major spectra, slot ring, barrier; x passes switch to [kx][z][y][3].
         // Symmetric (mirrored) tensor: real parity-reduced quarter Kp[kx][ky'][kz'][6];
         // otherwise (the reference's tensor via from_packed, or the unmirrored GPU
         // build) the full complex rows Kp[kx][ky][kz][6] (8x the bytes, no symmetry assumed)
+        // Slab (G ranks): planes [kx0, kx0 + kxn) of CHr per rank; the x passes write
+        // plane-major [kx][z_l][y][3] (CHr planes per all-to-all block, so each block
+        // is contiguous), and the pipeline reads the received [g][kx][z_l][y][3].
         const int L2 = pz / 2 + 1;
-        const size_t nk = symmetric ? (size_t)hx * L2 * L2 * 6 : (size_t)hx * pz * pz * 12;
+        const int CHr = G == 1 ? hx : (hx + G - 1) / G;
+        kx0 = rank * CHr;
+        kxn = std::max(0, std::min(CHr, hx - kx0));
+        const size_t np = (size_t)std::max(kxn, 1);
+        const size_t nk = symmetric ? np * L2 * L2 * 6 : np * pz * pz * 12;
         const size_t ns = (size_t)3 * g.nz * py * 3;
         MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
         MXB_CUDA(cudaMalloc(&slots, ns * sizeof(double2)));
         MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx + 3 * (size_t)g.nz) * sizeof(unsigned)));
-        int rc = symmetric ? pipe_quarter(K, Kp, pz, hx, hxp, st)
-                           : pipe_complex(K, reinterpret_cast<double2*>(Kp), pz, hx, hxp, st);
+        int rc = MXB_OK;
+        if (kxn > 0)
+            rc = symmetric ? pipe_quarter(K, Kp, pz, kxn, hxp, st, kx0)
+                           : pipe_complex(K, reinterpret_cast<double2*>(Kp), pz, kxn, hxp, st, kx0);
         if (rc) return rc;
         CH = 1;
         CHP = 1;
-        blk = (long long)g.nz * g.ny * 3;
+        blk = (long long)CHr * nz_l * g.ny * 3;
+        xblk = (long long)nz_l * g.ny * 3;
         kmode = symmetric ? 3 : 5;
         pipe = true;
         MXB_CUDA(cudaStreamSynchronize(st));
@@ -538,6 +553,7 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         CH = 1;
         CHP = 1;
         blk = (long long)g.nz * g.ny * 3;
+        xblk = blk;
         kmode = 4;
         longy = true;
         MXB_CUDA(cudaStreamSynchronize(st));
@@ -594,7 +610,7 @@ int DemagPlan::x_forward(const double* m, cudaStream_t st, const int* halt) {
         return longy_rm_to_pm(X2, XS, g.ny, g.nz, hx, hxp, st);
     }
     if (fast && px >= 4 && (nx % 2) == 0)
-        rc = fast_rows(true, px / 2, m, XS, nullptr, Nl, nx, nx / 2, CH, CHP, blk, rows, plm.tw,
+        rc = fast_rows(true, px / 2, m, XS, nullptr, Nl, nx, nx / 2, CH, CHP, xblk, rows, plm.tw,
                        plx.tw, st, halt);
     if (rc == -1) {
         if (G > 1) { set_error("no x kernel for this slab shape"); return MXB_EINVAL; }
@@ -609,7 +625,7 @@ int DemagPlan::x_inverse(double* h, cudaStream_t st, const int* halt) {
     const int nx = g.nx;
     int rc = -1;
     if (fast && px >= 4 && (nx % 2) == 0)
-        rc = fast_rows(false, px / 2, nullptr, XS, h, Nl, nx, nx / 2, CH, CHP, blk, rows, plm.tw,
+        rc = fast_rows(false, px / 2, nullptr, XS, h, Nl, nx, nx / 2, CH, CHP, xblk, rows, plm.tw,
                        plx.tw, st, halt);
     if (rc == -1) {
         if (G > 1) { set_error("no x kernel for this slab shape"); return MXB_EINVAL; }
@@ -628,7 +644,7 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
     if (kxn <= 0) { mark(2); mark(3); mark(4); return MXB_OK; }
     if (pipe) {
         mark(2);
-        rc = pipe_yz(XR, slots, Kp, bar, hx, nz, scale, plz.tw, st, halt, kmode == 5 ? 1 : 0);
+        rc = pipe_yz(XR, slots, Kp, bar, kxn, nz, scale, plz.tw, st, halt, kmode == 5 ? 1 : 0, nz_l, blk);
         mark(3);
         mark(4);
         return rc;

@@ -35,11 +35,13 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
 
 // L2-resident y/z pipeline over kx planes (yz_pipe.cu)
 bool pipe_shape_ok(int ny, int nz);
+// hx planes of XP (the rank's kx chunk); slab: XP = [g][hx][nzl][ny][3] blocks of gstride elements
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
-            const double2* tw, cudaStream_t st, const int* halt, int cplx);
-int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st);
+            const double2* tw, cudaStream_t st, const int* halt, int cplx, int nzl = 0, long long gstride = 0);
+// planes kx0 .. kx0+hx-1 of the full spectra K
+int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st, int kx0 = 0);
 bool pipe_cplx_ok(int L);
-int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st);
+int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st, int kx0 = 0);
 // long y lines (longy.cu)
 bool longy_shape_ok(int py);
 int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
@@ -59,6 +61,7 @@ struct DemagPlan {
     int G = 1, rank = 0, nz_l = 1, z0 = 0;
     int CH = 1, CHP = 8, kx0 = 0, kxn = 1;
     long long blk = 0;       // complex elements per all-to-all block
+    long long xblk = 0;      // the x passes' block stride (== blk, except the slab pipeline: one local plane)
     double2* XS = nullptr;   // x-pass side, [G][nz_l][ny][CHP][3] (send layout)
     double2* XR = nullptr;   // kx-chunk side, [nz][ny][CHP][3] (== XS for one rank)
     double2* X2 = nullptr;   // [nz][py][CHP][3]

@@ -73,7 +73,18 @@ struct PipeArgs {
     int hx, n;            // planes; non-zero rows ny == nz == n
     double scale;
     int cplx;             // 1: Kp holds full complex spectra [hx][L][L][6] (double2), no symmetry assumed
+    // z-slab decomposition (G ranks): XP is the all-to-all receive buffer
+    // [g][hx][nzl][ny][3] -- row z of plane p lives in block g = z / nzl.  One
+    // rank: nzl = n, a single block.
+    int nzl;
+    long long gstride;    // complex elements per source block
 };
+
+// first element of row z (y line, 3 components) of plane p in XP
+__device__ __forceinline__ long long xp_row(const PipeArgs& a, long long plane_xp, int p, int z, int rowlen) {
+    const int g = z / a.nzl;
+    return g * a.gstride + (long long)p * plane_xp + (long long)(z - g * a.nzl) * rowlen;
+}
 
 // H = K M for one kz element with complex K (the reference's own tensor, whose
 // spectra are not exactly real): k points at the six complex components
@@ -274,7 +285,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     double2* X = sm;
     double2* S = sm + PipeCfg<L>::XE;
     const int n = a.n, hx = a.hx;
-    const long long plane_xp = (long long)n * n * 3;       // XP elements per kx plane
+    const long long plane_xp = (long long)a.nzl * n * 3;       // XP elements per kx plane
     const long long slot_e = (long long)n * L * 3;         // slot elements
     const int b = threadIdx.x / TPL, t = threadIdx.x - (threadIdx.x / TPL) * TPL;
     const Sched sc(a, L, halt);
@@ -285,7 +296,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
     // own forward FFT
     auto stage_in = [&](const Unit& u) {
         if (u.kind == U_A) {
-            const double2* src = a.XP + u.plane * plane_xp + (long long)u.idx * n * 3;
+            const double2* src = a.XP + xp_row(a, plane_xp, u.plane, u.idx, n * 3);
             for (int j = threadIdx.x; j < 3 * n; j += T) cp_async16(&S[j], src + j, true);
         } else if (u.kind == U_B) {
             const double2* col = a.slot + (long long)(u.plane % 3) * slot_e + (long long)u.idx * 3;
@@ -422,7 +433,7 @@ k_yz_pipe(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ ha
                 if (e < n) X[e * 3 + b] = v[i];
             }
             __syncthreads();
-            double2* dst = a.XP + cur.plane * plane_xp + (long long)cur.idx * n * 3;
+            double2* dst = a.XP + xp_row(a, plane_xp, cur.plane, cur.idx, n * 3);
             for (int j = threadIdx.x; j < 3 * n; j += T) st_stream(dst + j, X[j]);
         }
         if (threadIdx.x == 0) {
@@ -460,7 +471,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     // warp's 32 consecutive kz rows are 1.5 KB contiguous)
     const double2* __restrict__ Kp2 = reinterpret_cast<const double2*>(a.Kp);
     const int hx = a.hx;
-    const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
+    const long long plane_xp = (long long)a.nzl * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * L;
     const Sched sc(a, L, halt);
@@ -476,9 +487,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         if (u.kind == U_A) {
 #if MXB_PIPE_BULK
             if (threadIdx.x == 0)
-                bulk_g2s(W, a.XP + u.plane * plane_xp + (long long)u.idx * N * 3, 3 * N * 16, &mbar);
+                bulk_g2s(W, a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3), 3 * N * 16, &mbar);
 #else
-            const double2* src = a.XP + u.plane * plane_xp + (long long)u.idx * N * 3;
+            const double2* src = a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3);
             for (int j = threadIdx.x; j < 3 * N; j += 96) cp_async16(&W[j], src + j, true);
 #endif
         } else if (u.kind == U_B) {
@@ -674,11 +685,11 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 // ---- y inverse of row z = idx -> XP row (n of L kept)
                 if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
 #if MXB_PIPE_W_DIRECT_STORE
-                double2* dst = a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3 + c;
+                double2* dst = a.XP + xp_row(a, plane_xp, cur.plane, cur.idx, N * 3) + c;
 #pragma unroll
                 for (int k = 0; k < 16; ++k) st_stream(dst + (long long)(lane + 32 * k) * 3, v[fw::p32(k)]);
 #else
-                store_rows(v, std::integral_constant<int, 16>{}, a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3,
+                store_rows(v, std::integral_constant<int, 16>{}, a.XP + xp_row(a, plane_xp, cur.plane, cur.idx, N * 3),
                            N, true, lane);
 #endif
             } else {
@@ -743,7 +754,7 @@ k_yz_pipe_wq(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__
     double2* Q = sm + 3 * L;      // 3 x 512: the next A / B unit's input
     const double2* __restrict__ Kp2 = reinterpret_cast<const double2*>(a.Kp);
     const int hx = a.hx;
-    const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
+    const long long plane_xp = (long long)a.nzl * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * L;
     const Sched sc(a, L, halt);
@@ -753,7 +764,7 @@ k_yz_pipe_wq(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__
     auto issue = [&](const Unit& u, double2* dst, unsigned long long* mb) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         if (u.kind == U_A) {
-            bulk_g2s(dst, a.XP + u.plane * plane_xp + (long long)u.idx * N * 3, 3 * N * 16, mb);
+            bulk_g2s(dst, a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3), 3 * N * 16, mb);
         } else if (u.kind == U_B) {
             mbar_expect(mb, 2 * 256 * 48);
             const int y0 = (u.plane % 3) * N;
@@ -893,7 +904,7 @@ k_yz_pipe_wq(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__
             if (threadIdx.x == 0) {
                 if (cur.kind == U_C) {
                     // ---- y inverse of row z = idx -> XP row: one bulk store
-                    bulk_store(a.XP + cur.plane * plane_xp + (long long)cur.idx * N * 3, 3 * N);
+                    bulk_store(a.XP + xp_row(a, plane_xp, cur.plane, cur.idx, N * 3), 3 * N);
                 } else {
                     // ---- B: the column back into the slot as two tensor boxes
                     const int y0 = (cur.plane % 3) * N;
@@ -935,7 +946,7 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
     __shared__ int flag;
     __shared__ alignas(8) unsigned long long mbar;  // bulk row copies (A, C)
     const int hx = a.hx;
-    const long long plane_xp = (long long)N * N * 3, slot_e = (long long)N * L * 3;
+    const long long plane_xp = (long long)a.nzl * N * 3, slot_e = (long long)N * L * 3;
     const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* Wc = W + c * 1024;
     PipeArgs au = a;
@@ -948,7 +959,7 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
         double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
         if (u.kind == U_A) {   // rows 2 idx, 2 idx + 1 of XP: contiguous
             if (threadIdx.x == 0)
-                bulk_g2s(W, a.XP + u.plane * plane_xp + (long long)(2 * u.idx) * N * 3, 2 * N * 3 * 16, &mbar);
+                bulk_g2s(W, a.XP + xp_row(a, plane_xp, u.plane, 2 * u.idx, N * 3), 2 * N * 3 * 16, &mbar);
         } else if (u.kind == U_B) {   // columns 2 idx, 2 idx + 1: 96 contiguous bytes per z
             const int ky0 = 2 * u.idx;
             for (int j = threadIdx.x; j < 6 * N; j += 96) {
@@ -1083,7 +1094,7 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
             __syncthreads();
             if (cur.kind == U_C) {
                 // ---- y inverse of rows 2 idx (+1) -> XP rows (contiguous)
-                double2* dst = a.XP + cur.plane * plane_xp + (long long)(2 * cur.idx) * N * 3;
+                double2* dst = a.XP + xp_row(a, plane_xp, cur.plane, 2 * cur.idx, N * 3);
                 for (int j = threadIdx.x; j < 2 * N * 3; j += 96) st_stream(dst + j, W[j]);
             } else {
                 // ---- B: columns back into the slot (96 contiguous bytes per z)
@@ -1267,8 +1278,9 @@ bool pipe_cplx_ok(int L) {
 }
 
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
-            const double2* tw, cudaStream_t st, const int* halt, int cplx) {
-    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale, cplx};
+            const double2* tw, cudaStream_t st, const int* halt, int cplx, int nzl, long long gstride) {
+    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale, cplx, nzl > 0 ? nzl : n, gstride};
+    if (a.nzl != n && (a.nzl % 2 || n % a.nzl)) { set_error("pipeline slab: local planes must be even and divide n"); return MXB_EINVAL; }
     if (cplx && !pipe_cplx_ok(2 * n)) { set_error("complex-spectra pipeline needs the warp kernels (L = 512 / 1024)"); return MXB_EINVAL; }
     // warp-FFT variant by default at L = 1024 (27.6 vs 32.1 ms per evaluation at
     // 512^3; within 4e-16 of the 5-pass path).  MXB_PIPE_WARP=0 selects the
@@ -1295,7 +1307,7 @@ int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx,
 
 // K (complex full spectra [kz][ky][hxp][6], exactly real) -> Kp[kx][ky'][kz'][6]
 __global__ void k_planes_quarter(const double2* __restrict__ K, double* __restrict__ Kp, int L, int hx,
-                                 int hxp) {
+                                 int hxp, int kx0) {
     const int L2 = L / 2 + 1;
     const long long tot = (long long)hx * L2 * L2 * 6;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
@@ -1306,12 +1318,12 @@ __global__ void k_planes_quarter(const double2* __restrict__ K, double* __restri
         r /= L2;
         const int ky = (int)(r % L2);
         const int kx = (int)(r / L2);
-        Kp[i] = K[(((long long)kz * L + ky) * hxp + kx) * 6 + c].x;
+        Kp[i] = K[(((long long)kz * L + ky) * hxp + kx0 + kx) * 6 + c].x;
     }
 }
 
-int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st) {
-    k_planes_quarter<<<148 * 8, 256, 0, st>>>(K, Kp, L, hx, hxp);
+int pipe_quarter(const double2* K, double* Kp, int L, int hx, int hxp, cudaStream_t st, int kx0) {
+    k_planes_quarter<<<148 * 8, 256, 0, st>>>(K, Kp, L, hx, hxp, kx0);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
@@ -1322,7 +1334,8 @@ namespace mxb {
 
 // K (complex full spectra [kz][ky][hxp][6]) -> Kx[kx][ky][kz][6] complex, the
 // B units' kernel rows contiguous (L x 96 B per (kx, ky))
-__global__ void k_planes_complex(const double2* __restrict__ K, double2* __restrict__ Kx, int L, int hx, int hxp) {
+__global__ void k_planes_complex(const double2* __restrict__ K, double2* __restrict__ Kx, int L, int hx, int hxp,
+                                 int kx0) {
     const long long tot = (long long)hx * L * L * 6;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
          i += (long long)gridDim.x * blockDim.x) {
@@ -1332,12 +1345,12 @@ __global__ void k_planes_complex(const double2* __restrict__ K, double2* __restr
         r /= L;
         const int ky = (int)(r % L);
         const int kx = (int)(r / L);
-        Kx[i] = K[(((long long)kz * L + ky) * hxp + kx) * 6 + c];
+        Kx[i] = K[(((long long)kz * L + ky) * hxp + kx0 + kx) * 6 + c];
     }
 }
 
-int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st) {
-    k_planes_complex<<<148 * 8, 256, 0, st>>>(K, Kx, L, hx, hxp);
+int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStream_t st, int kx0) {
+    k_planes_complex<<<148 * 8, 256, 0, st>>>(K, Kx, L, hx, hxp, kx0);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }

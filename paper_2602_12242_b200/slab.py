@@ -179,7 +179,11 @@ class CudaSlabBackend:
             L.check(lib.mxb_demag_set_stream(self.d, C.c_void_p(self.stream)))
             s, r = C.c_void_p(), C.c_void_p()
             L.check(lib.mxb_demag_slab_buffers(self.d, C.byref(s), C.byref(r)))
-            n = 2 * plan.nranks * plan.block_elems
+            blk = C.c_int64()
+            L.check(lib.mxb_demag_slab_block(self.d, C.byref(blk)))
+            # row-major kx chunks (plan.block_elems) or, with the plane pipeline,
+            # plane-major chunks of whole kx planes
+            n = 2 * plan.nranks * int(blk.value)
             self.send = torch.as_tensor(_CudaArray(s.value, n), device=self.dev)
             self.recv = torch.as_tensor(_CudaArray(r.value, n), device=self.dev)
 

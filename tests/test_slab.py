@@ -17,6 +17,9 @@ from oracle import magnex_oracle as O
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 NX, NY, NZ = 16, 8, 8
+# grids of the plane-pipeline slab cases (ny == nz; MXB_PIPE=1 forces the pipeline):
+# radix-16 core (L = 32), warp pair core (L = 512), warp core (L = 1024, the bench's)
+PIPE_DIMS = {"pipe": (16, 16, 16), "pipe512": (8, 256, 256), "pipe1024": (8, 512, 512)}
 CELL = (2e-9, 2.5e-9, 3e-9)
 DT = 2e-14
 NSTEPS = 3
@@ -29,6 +32,10 @@ def free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def dims_of(case):
+    return PIPE_DIMS.get(case, (NX, NY, NZ))
 
 
 def _disk_ms():
@@ -50,11 +57,12 @@ def _mat_kw(case):
 
 
 def problem(case="uniform"):
+    nx, ny, nz = dims_of(case)
     ms, kw = _mat_kw(case)
-    mat = O.make_mat((NX, NY, NZ), CELL, ms, **kw)
+    mat = O.make_mat((nx, ny, nz), CELL, ms, **kw)
     rng = np.random.default_rng(21)
-    m0 = O.renormalize(rng.normal(size=(3, NZ, NY, NX)), mat)
-    packed = O.packed_tensor(NX, NY, NZ, *CELL)
+    m0 = O.renormalize(rng.normal(size=(3, nz, ny, nx)), mat)
+    packed = O.packed_tensor(nx, ny, nz, *CELL)
     return mat, m0, packed
 
 
@@ -64,6 +72,17 @@ def reference(case="uniform"):
     terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=O.kernel_spectra(packed),
                     bias=np.array(BIAS), cubic=extra, bulk_dmi=extra)
     return O.run(m0, mat, terms, "rk4", DT, max_steps=NSTEPS, sample_every=1)
+
+
+def reference_state(case):
+    """the single-domain result (cached per case: the large pipeline grids take
+    seconds per oracle evaluation)"""
+    if case not in _REF:
+        _REF[case] = reference(case)
+    return _REF[case]
+
+
+_REF = {}
 
 
 def _terms(case="uniform"):
@@ -78,10 +97,13 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if case in PIPE_DIMS:
+        os.environ["MXB_PIPE"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2602_12242_b200.slab import Comm, SlabPlan, SlabSimulation
     mat, m0, packed = problem(case)
-    plan = SlabPlan(NX, NY, NZ, world, rank)
+    NX_, NY_, NZ_ = dims_of(case)
+    plan = SlabPlan(NX_, NY_, NZ_, world, rank)
     z0, nzl = plan.z0, plan.nz_local
     terms = _terms(case)
     if kind == "numpy":
@@ -94,15 +116,19 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
         from paper_2602_12242_b200 import _lib as L
         from paper_2602_12242_b200.slab import CudaSlabBackend
         torch.cuda.set_device(0)
-        gl = mx.GridSpec(NX, NY, nzl, *CELL)
+        gl = mx.GridSpec(NX_, NY_, nzl, *CELL)
         ms, kw = _mat_kw(case)
         sl = (lambda a: a[z0:z0 + nzl] if np.ndim(a) == 3 else a)  # noqa: E731
         kw = {k: sl(v) for k, v in kw.items()}
         mat_l = mx.MaterialMap(gl, Ms=sl(ms), **kw)
         h = C.c_void_p()
-        L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(NX, NY, NZ, *CELL)._c()), 0, world,
+        L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(NX_, NY_, NZ_, *CELL)._c()), 0, world,
                                                rank, C.byref(h)))
         L.check(L.load().mxb_demag_set_packed(h, L.dptr(np.ascontiguousarray(packed))))
+        km = C.c_int()
+        L.check(L.load().mxb_demag_kmode(h, C.byref(km)))
+        if case in PIPE_DIMS:
+            assert km.value == 5, km.value      # reference tensor: complex-spectra plane pipeline
         b = CudaSlabBackend(plan, gl, mat_l, h, 0)
     sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=DT, bias=BIAS, check_every=check_every)
     sim.start(m0[:, z0:z0 + nzl])
@@ -145,11 +171,13 @@ def test_slab_numpy_gloo_matches_single_domain(case, check_every):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["uniform", "disk"])
+@pytest.mark.parametrize("case", ["uniform", "disk", "pipe", "pipe512", "pipe1024"])
 def test_slab_cuda_two_ranks_match_single_domain(case):
     """disk: per-cell Ms and A across the slab faces (the neighbours' material
-    planes are swapped once at start), cubic anisotropy and bulk DMI."""
-    ref = reference(case)
+    planes are swapped once at start), cubic anisotropy and bulk DMI.
+    pipe*: the y/z plane pipeline on each rank's kx chunk, reading the
+    all-to-all receive blocks in place (plane-major chunks)."""
+    ref = reference_state(case)
     state, steps, mean0, status, mean1 = _run("cuda", case)
     assert steps == NSTEPS and status == 0
     assert np.max(np.abs(state - ref.m)) <= 1e-11 * 8e5
