@@ -60,6 +60,23 @@
 #ifndef MXB_PIPE_W_DIRECT_STORE
 #define MXB_PIPE_W_DIRECT_STORE 0
 #endif
+// per-access L2 eviction hints in k_yz_pipe_w: 0 none; 1 slot ring evict_last,
+// XP rows / kernel rows evict_first; 2 only the streams evict_first
+#ifndef MXB_PIPE_HINTS
+#define MXB_PIPE_HINTS 0
+#endif
+#ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too
+#define MXB_PIPE_HINT_K 0
+#endif
+#if MXB_PIPE_HINTS
+#define PIPE_POL_STREAM() policy_evict_first()
+#if MXB_PIPE_HINTS == 1
+#define PIPE_SLOT_HINTED 1
+#define PIPE_POL_SLOT() policy_evict_last()
+#else
+#define PIPE_SLOT_HINTED 0
+#endif
+#endif
 
 namespace mxb {
 
@@ -486,8 +503,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #endif
         if (u.kind == U_A) {
 #if MXB_PIPE_BULK
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0) {
+#if MXB_PIPE_HINTS
+                bulk_g2s_hint(W, a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3), 3 * N * 16, &mbar,
+                              PIPE_POL_STREAM());
+#else
                 bulk_g2s(W, a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3), 3 * N * 16, &mbar);
+#endif
+            }
 #else
             const double2* src = a.XP + xp_row(a, plane_xp, u.plane, u.idx, N * 3);
             for (int j = threadIdx.x; j < 3 * N; j += 96) cp_async16(&W[j], src + j, true);
@@ -499,8 +522,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 mbar_expect(&mbar, 2 * 256 * 48);
                 const int y0 = (u.plane % 3) * N;
+#if MXB_PIPE_HINTS && PIPE_SLOT_HINTED
+                const unsigned long long ps = PIPE_POL_SLOT();
+                tma_load_2d_hint(W, &tmap_slot, u.idx * 6, y0, &mbar, ps);
+                tma_load_2d_hint(W + 768, &tmap_slot, u.idx * 6, y0 + 256, &mbar, ps);
+#else
                 tma_load_2d(W, &tmap_slot, u.idx * 6, y0, &mbar);
                 tma_load_2d(W + 768, &tmap_slot, u.idx * 6, y0 + 256, &mbar);
+#endif
             }
 #else
             const double2* col = slot + (long long)u.idx * 3;
@@ -518,14 +547,22 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 } else {
                     const int kyq = 2 * u.idx > L ? L - u.idx : u.idx;
                     const double* kr = a.Kp + ((long long)u.plane * L2 + kyq) * L2 * 6;
+#if MXB_PIPE_HINTS
+                    prefetch_l2_hint(kr, L2 * 48, PIPE_POL_STREAM());
+#else
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kr), "r"(L2 * 48) : "memory");
+#endif
                 }
             }
         } else {
 #if MXB_PIPE_BULK
             if (threadIdx.x == 0) {
                 asm volatile("fence.proxy.async.global;" ::: "memory");
+#if MXB_PIPE_HINTS
+                bulk_g2s_hint(W, slot + (long long)u.idx * L * 3, 3 * L * 16, &mbar, PIPE_POL_STREAM());
+#else
                 bulk_g2s(W, slot + (long long)u.idx * L * 3, 3 * L * 16, &mbar);
+#endif
             }
 #else
             const double2* src = slot + (long long)u.idx * L * 3;
@@ -555,13 +592,27 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #if MXB_PIPE_TMA
         // one bulk store of the contiguous row (the next unit stages into W, so
         // the store must have read it before the end-of-unit barrier)
+#if !MXB_PIPE_HINTS
         (void)stream;
+#endif
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (threadIdx.x == 0) {
+#if MXB_PIPE_HINTS
+            if (stream)
+                bulk_s2g_hint(dst, W, 3 * ne * 16, PIPE_POL_STREAM());
+#if PIPE_SLOT_HINTED
+            else
+                bulk_s2g_hint(dst, W, 3 * ne * 16, PIPE_POL_SLOT());
+#else
+            else
+                bulk_s2g(dst, W, 3 * ne * 16);
+#endif
+#else
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                          "r"(smem_u32(W)), "r"(3 * ne * 16)
                          : "memory");
+#endif
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 #if !MXB_PIPE_LATE_READ_WAIT
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -652,11 +703,18 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                         kmul_complex(krow + kz * 6, W[kz], W[L + kz], W[2 * L + kz], s);
                 }
                 const double2* krow = Kp2 + ((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 * 3;
+#if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                const unsigned long long pk = PIPE_POL_STREAM();
+#endif
                 // each thread owns whole kz rows (all 3 components), in place in W
                 for (int kz = a.cplx ? L : threadIdx.x; kz < L; kz += 96) {
                     const bool fz = 2 * kz > L;
                     const double2* kr = krow + (fz ? L - kz : kz) * 3;
+#if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                    const double2 q01 = ldg_hint(kr, pk), q23 = ldg_hint(kr + 1, pk), q45 = ldg_hint(kr + 2, pk);
+#else
                     const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
+#endif
                     const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
                     const double kxy = fy ? -q01.y : q01.y;
                     const double kxz = fz ? -q23.x : q23.x;
@@ -702,8 +760,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     const int y0 = (cur.plane % 3) * N;
+#if MXB_PIPE_HINTS && PIPE_SLOT_HINTED
+                    const unsigned long long ps = PIPE_POL_SLOT();
+                    tma_store_2d_hint(&tmap_slot, cur.idx * 6, y0, W, ps);
+                    tma_store_2d_hint(&tmap_slot, cur.idx * 6, y0 + 256, W + 768, ps);
+#else
                     tma_store_2d(&tmap_slot, cur.idx * 6, y0, W);
                     tma_store_2d(&tmap_slot, cur.idx * 6, y0 + 256, W + 768);
+#endif
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     // W is staged into by the next unit: the stores must have read it
                     // (waited for in the next stage(), or here)
