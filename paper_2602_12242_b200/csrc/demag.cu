@@ -366,7 +366,7 @@ bool DemagPlan::pipe_candidate(bool symmetric) const {
     if (pz <= 1 || py <= 1 || !fast) return false;
     // z slab: the pipeline runs on the rank's kx chunk of all nz planes, read in
     // place from the all-to-all receive blocks (pairs of rows need even nz_l)
-    if (G > 1 && (nz_l % 2)) return false;
+    if (G > 1 && (nz_l < 2 || (nz_l & (nz_l - 1)))) return false;
     if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
     if (!pipe_shape_ok(g.ny, g.nz)) return false;
     if (!symmetric && !pipe_cplx_ok(pz)) return false;

@@ -65,6 +65,9 @@
 #ifndef MXB_PIPE_HINTS
 #define MXB_PIPE_HINTS 0
 #endif
+#ifndef MXB_PIPE_KPAIR      // B multiply: one kernel-entry load for kz and L - kz
+#define MXB_PIPE_KPAIR 0
+#endif
 #ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too
 #define MXB_PIPE_HINT_K 0
 #endif
@@ -93,14 +96,14 @@ struct PipeArgs {
     // z-slab decomposition (G ranks): XP is the all-to-all receive buffer
     // [g][hx][nzl][ny][3] -- row z of plane p lives in block g = z / nzl.  One
     // rank: nzl = n, a single block.
-    int nzl;
-    long long gstride;    // complex elements per source block
+    int nzl;              // a power of two
+    long long zjump;      // source block stride / nzl (elements per z of the block index)
 };
 
 // first element of row z (y line, 3 components) of plane p in XP
 __device__ __forceinline__ long long xp_row(const PipeArgs& a, long long plane_xp, int p, int z, int rowlen) {
-    const int g = z / a.nzl;
-    return g * a.gstride + (long long)p * plane_xp + (long long)(z - g * a.nzl) * rowlen;
+    const int zl = z & (a.nzl - 1);
+    return (long long)(z - zl) * a.zjump + (long long)p * plane_xp + (long long)zl * rowlen;
 }
 
 // H = K M for one kz element with complex K (the reference's own tensor, whose
@@ -707,6 +710,35 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 const unsigned long long pk = PIPE_POL_STREAM();
 #endif
                 // each thread owns whole kz rows (all 3 components), in place in W
+#if MXB_PIPE_KPAIR
+                // kz and L - kz share the parity-reduced entry kz' = min(kz, L - kz):
+                // each entry is loaded once and applied to both (sign flip of XZ, YZ)
+                for (int q = a.cplx ? L : threadIdx.x; q <= L / 2; q += 96) {
+                    const double2* kr = krow + q * 3;
+#if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                    const double2 q01 = ldg_hint(kr, pk), q23 = ldg_hint(kr + 1, pk), q45 = ldg_hint(kr + 2, pk);
+#else
+                    const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
+#endif
+                    const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                    const double kxy = fy ? -q01.y : q01.y;
+                    auto apply = [&](int kz, double kxz, double kyz) {
+                        const double2 m0 = W[kz], m1 = W[L + kz], m2 = W[2 * L + kz];
+                        const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                        kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                        const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                        kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                        const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                        kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                        W[kz] = make_double2(h0.x * s, h0.y * s);
+                        W[L + kz] = make_double2(h1.x * s, h1.y * s);
+                        W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
+                    };
+                    const double kyz0 = fy ? -q45.x : q45.x;
+                    apply(q, q23.x, kyz0);
+                    if (q != 0 && q != L / 2) apply(L - q, -q23.x, -kyz0);
+                }
+#else
                 for (int kz = a.cplx ? L : threadIdx.x; kz < L; kz += 96) {
                     const bool fz = 2 * kz > L;
                     const double2* kr = krow + (fz ? L - kz : kz) * 3;
@@ -730,6 +762,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                     W[L + kz] = make_double2(h1.x * s, h1.y * s);
                     W[2 * L + kz] = make_double2(h2.x * s, h2.y * s);
                 }
+#endif
                 __syncthreads();
 #pragma unroll
                 for (int m = 0; m < 32; ++m) v[m] = Wc[lane + 32 * m];
@@ -1343,8 +1376,12 @@ bool pipe_cplx_ok(int L) {
 
 int pipe_yz(double2* XP, double2* slot, const double* Kp, unsigned* bar, int hx, int n, double scale,
             const double2* tw, cudaStream_t st, const int* halt, int cplx, int nzl, long long gstride) {
-    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale, cplx, nzl > 0 ? nzl : n, gstride};
-    if (a.nzl != n && (a.nzl % 2 || n % a.nzl)) { set_error("pipeline slab: local planes must be even and divide n"); return MXB_EINVAL; }
+    const int nzl_ = nzl > 0 ? nzl : n;
+    const PipeArgs a{XP, slot, Kp, bar, hx, n, scale, cplx, nzl_, nzl_ != n ? gstride / nzl_ : 0};
+    if (a.nzl != n && (a.nzl < 2 || (a.nzl & (a.nzl - 1)) || n % a.nzl || gstride % a.nzl)) {
+        set_error("pipeline slab: the local planes must be a power of two dividing n");
+        return MXB_EINVAL;
+    }
     if (cplx && !pipe_cplx_ok(2 * n)) { set_error("complex-spectra pipeline needs the warp kernels (L = 512 / 1024)"); return MXB_EINVAL; }
     // warp-FFT variant by default at L = 1024 (27.6 vs 32.1 ms per evaluation at
     // 512^3; within 4e-16 of the 5-pass path).  MXB_PIPE_WARP=0 selects the
