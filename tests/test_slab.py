@@ -137,8 +137,7 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
     dist.destroy_process_group()
 
 
-def _run(kind, case="uniform", check_every=16):
-    world = 2
+def _run(kind, case="uniform", check_every=16, world=2):
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(world, free_port(), kind, out, case, check_every), nprocs=world,
@@ -160,10 +159,11 @@ def test_slab_plan_chunks_cover_the_spectrum():
         SlabPlan(8, 8, 6, 4, 0)
 
 
-@pytest.mark.parametrize("case,check_every", [("uniform", 16), ("uniform", 1), ("disk", 2)])
-def test_slab_numpy_gloo_matches_single_domain(case, check_every):
+@pytest.mark.parametrize("case,check_every,world", [("uniform", 16, 2), ("uniform", 1, 2), ("disk", 2, 2),
+                                                    ("disk", 16, 4)])
+def test_slab_numpy_gloo_matches_single_domain(case, check_every, world):
     ref = reference(case)
-    state, steps, mean0, status, mean1 = _run("numpy", case, check_every)
+    state, steps, mean0, status, mean1 = _run("numpy", case, check_every, world)
     assert steps == NSTEPS and status == 0
     assert np.max(np.abs(state - ref.m)) <= 1e-12 * 8e5
     assert np.array_equal(mean0, mean1)              # every rank committed the same step
@@ -171,14 +171,15 @@ def test_slab_numpy_gloo_matches_single_domain(case, check_every):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["uniform", "disk", "pipe", "pipe512", "pipe1024"])
-def test_slab_cuda_two_ranks_match_single_domain(case):
+@pytest.mark.parametrize("case,world", [("uniform", 2), ("disk", 2), ("disk", 4), ("pipe", 2), ("pipe", 4),
+                                        ("pipe512", 2), ("pipe1024", 2), ("pipe1024", 4)])
+def test_slab_cuda_ranks_match_single_domain(case, world):
     """disk: per-cell Ms and A across the slab faces (the neighbours' material
     planes are swapped once at start), cubic anisotropy and bulk DMI.
     pipe*: the y/z plane pipeline on each rank's kx chunk, reading the
     all-to-all receive blocks in place (plane-major chunks)."""
     ref = reference_state(case)
-    state, steps, mean0, status, mean1 = _run("cuda", case)
+    state, steps, mean0, status, mean1 = _run("cuda", case, world=world)
     assert steps == NSTEPS and status == 0
     assert np.max(np.abs(state - ref.m)) <= 1e-11 * 8e5
     assert np.array_equal(mean0, mean1)
