@@ -19,7 +19,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NX, NY, NZ = 16, 8, 8
 # grids of the plane-pipeline slab cases (ny == nz; MXB_PIPE=1 forces the pipeline):
 # radix-16 core (L = 32), warp pair core (L = 512), warp core (L = 1024, the bench's)
-PIPE_DIMS = {"pipe": (16, 16, 16), "pipe512": (8, 256, 256), "pipe1024": (8, 512, 512)}
+# pipe512 / pipe1024 run the reference's tensor (complex-spectra pipeline, kernel
+# mode 5); pipe1024sym the mirrored GPU build (kernel mode 3, the bench's mode),
+# checked against the single-domain oracle on the spectra of the same build
+PIPE_DIMS = {"pipe512": (8, 256, 256), "pipe1024": (8, 512, 512), "pipe1024sym": (8, 512, 512)}
 CELL = (2e-9, 2.5e-9, 3e-9)
 DT = 2e-14
 NSTEPS = 3
@@ -66,10 +69,16 @@ def problem(case="uniform"):
     return mat, m0, packed
 
 
+def _sym_spectra(case):
+    import paper_2602_12242_b200 as mx
+    return mx.DemagKernel.build(mx.GridSpec(*dims_of(case), *CELL), symmetric=True).spectra
+
+
 def reference(case="uniform"):
     mat, m0, packed = problem(case)
     extra = case == "disk"
-    terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=O.kernel_spectra(packed),
+    spectra = _sym_spectra(case) if case.endswith("sym") else O.kernel_spectra(packed)
+    terms = O.Terms(exchange=True, anisotropy=True, dmi=True, spectra=spectra,
                     bias=np.array(BIAS), cubic=extra, bulk_dmi=extra)
     return O.run(m0, mat, terms, "rk4", DT, max_steps=NSTEPS, sample_every=1)
 
@@ -124,11 +133,15 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
         h = C.c_void_p()
         L.check(L.load().mxb_demag_create_slab(C.byref(mx.GridSpec(NX_, NY_, NZ_, *CELL)._c()), 0, world,
                                                rank, C.byref(h)))
-        L.check(L.load().mxb_demag_set_packed(h, L.dptr(np.ascontiguousarray(packed))))
+        if case.endswith("sym"):
+            L.check(L.load().mxb_demag_build(h, 1))
+        else:
+            L.check(L.load().mxb_demag_set_packed(h, L.dptr(np.ascontiguousarray(packed))))
         km = C.c_int()
         L.check(L.load().mxb_demag_kmode(h, C.byref(km)))
         if case in PIPE_DIMS:
-            assert km.value == 5, km.value      # reference tensor: complex-spectra plane pipeline
+            # plane pipeline: mirrored build -> real quarter (3), reference tensor -> complex (5)
+            assert km.value == (3 if case.endswith("sym") else 5), km.value
         b = CudaSlabBackend(plan, gl, mat_l, h, 0)
     sim = SlabSimulation(plan, b, Comm(), terms, method="rk4", dt=DT, bias=BIAS, check_every=check_every)
     sim.start(m0[:, z0:z0 + nzl])
@@ -171,8 +184,8 @@ def test_slab_numpy_gloo_matches_single_domain(case, check_every, world):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("uniform", 2), ("disk", 2), ("disk", 4), ("pipe", 2), ("pipe", 4),
-                                        ("pipe512", 2), ("pipe1024", 2), ("pipe1024", 4)])
+@pytest.mark.parametrize("case,world", [("uniform", 2), ("disk", 2), ("disk", 4), ("pipe512", 2), ("pipe512", 4),
+                                        ("pipe1024", 2), ("pipe1024sym", 2), ("pipe1024sym", 4)])
 def test_slab_cuda_ranks_match_single_domain(case, world):
     """disk: per-cell Ms and A across the slab faces (the neighbours' material
     planes are swapped once at start), cubic anisotropy and bulk DMI.
