@@ -61,12 +61,17 @@
 #define MXB_PIPE_W_DIRECT_STORE 0
 #endif
 // per-access L2 eviction hints in k_yz_pipe_w: 0 none; 1 slot ring evict_last,
-// XP rows / kernel rows evict_first; 2 only the streams evict_first
+// XP rows / kernel rows evict_first; 2 only the streams evict_first.
+// Measured at 512^3 (profiles/round2_pipe_hints_ab.md): with the kz-pair kernel
+// loads, 1 gives 20.13 ms per evaluation (DRAM 36.8 GB) vs 21.08 ms (49.1 GB)
 #ifndef MXB_PIPE_HINTS
-#define MXB_PIPE_HINTS 0
+#define MXB_PIPE_HINTS 1
 #endif
 #ifndef MXB_PIPE_KPAIR      // B multiply: one kernel-entry load for kz and L - kz
-#define MXB_PIPE_KPAIR 0
+#define MXB_PIPE_KPAIR 1
+#endif
+#ifndef MXB_PIPE_KPAIR_512  // the same in the L = 512 pair kernel (A/B, spills at 168 registers)
+#define MXB_PIPE_KPAIR_512 0
 #endif
 #ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too
 #define MXB_PIPE_HINT_K 0
@@ -1151,6 +1156,32 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
                                      W[2048 + t], s);
                     }
                 }
+#if MXB_PIPE_KPAIR_512
+                // kz and L - kz share a parity-reduced entry: one load, two updates
+                for (int t = a.cplx ? 2 * L2 : threadIdx.x; t < 2 * L2; t += 96) {
+                    const int ln = t / L2, q = t - ln * L2, ky = ky0 + ln;
+                    const bool fy = 2 * ky > L;
+                    const double2* kr = Kp2 + (((long long)cur.plane * L2 + (fy ? L - ky : ky)) * L2 + q) * 3;
+                    const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
+                    const double kxx = q01.x, kyy = q23.y, kzz = q45.y;
+                    const double kxy = fy ? -q01.y : q01.y;
+                    const double kyz0 = fy ? -q45.x : q45.x;
+                    auto apply = [&](int e, double kxz, double kyz) {
+                        const double2 m0 = W[e], m1 = W[1024 + e], m2 = W[2048 + e];
+                        const double2 h0 = make_double2(kxx * m0.x + kxy * m1.x + kxz * m2.x,
+                                                        kxx * m0.y + kxy * m1.y + kxz * m2.y);
+                        const double2 h1 = make_double2(kxy * m0.x + kyy * m1.x + kyz * m2.x,
+                                                        kxy * m0.y + kyy * m1.y + kyz * m2.y);
+                        const double2 h2 = make_double2(kxz * m0.x + kyz * m1.x + kzz * m2.x,
+                                                        kxz * m0.y + kyz * m1.y + kzz * m2.y);
+                        W[e] = make_double2(h0.x * s, h0.y * s);
+                        W[1024 + e] = make_double2(h1.x * s, h1.y * s);
+                        W[2048 + e] = make_double2(h2.x * s, h2.y * s);
+                    };
+                    apply(ln * L + q, q23.x, kyz0);
+                    if (q != 0 && q != L / 2) apply(ln * L + L - q, -q23.x, -kyz0);
+                }
+#else
                 for (int t = a.cplx ? 2 * L : threadIdx.x; t < 2 * L; t += 96) {
                     const int ln = t / L, kz = t - ln * L, ky = ky0 + ln;
                     const bool fy = 2 * ky > L, fz = 2 * kz > L;
@@ -1172,6 +1203,7 @@ k_yz_pipe_w512(PipeArgs a, const double2* __restrict__ tw, const int* __restrict
                     W[1024 + t] = make_double2(h1.x * s, h1.y * s);
                     W[2048 + t] = make_double2(h2.x * s, h2.y * s);
                 }
+#endif
                 __syncthreads();
 #pragma unroll
                 for (int m = 0; m < 16; ++m) {
