@@ -296,6 +296,11 @@ void mxb_fno_destroy(mxb_fno* f);
 int mxb_fno_infer(mxb_fno* f, const double* x, double* y);
 /* device pointers, on the model's stream (synchronise before reading y) */
 int mxb_fno_infer_dev(mxb_fno* f, const double* x, double* y);
+/* a demag handle whose field is the surrogate's forward pass (FnoDemag.field,
+ * fno.py:427-447): usable wherever an mxb_demag is, including mxb_run, where
+ * the forward pass runs inside the fused device step.  The film must be the
+ * model's H x W with nz = 1; f must outlive the handle. */
+int mxb_demag_create_fno(const mxb_grid* g, int device, mxb_fno* f, mxb_demag** out);
 /* spectral_conv (fno.py:228-255) of host (channels, ny, nx); w_pos/w_neg
  * (channels, channels, m1, m2) complex as (re, im) pairs */
 int mxb_fno_spectral_conv(int device, int channels, int ny, int nx, int m1, int m2,

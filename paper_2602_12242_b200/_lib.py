@@ -126,6 +126,7 @@ SIGNATURES = {
     "mxb_fno_destroy": ([C.c_void_p], None),
     "mxb_fno_infer": ([C.c_void_p, _dp, _dp], C.c_int),
     "mxb_fno_infer_dev": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "mxb_demag_create_fno": ([C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "mxb_fno_spectral_conv": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp],
                               C.c_int),
 }

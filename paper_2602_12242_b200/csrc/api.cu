@@ -37,8 +37,13 @@ using namespace mxb;
 
 static uint64_t g_demag_uid = 0;
 
+namespace mxb {
+int fno_forward_on(mxb_fno* h, const double* x, double* y, cudaStream_t st, int* H, int* W);
+}
+
 struct mxb_demag {
     DemagPlan plan;
+    mxb_fno* fno = nullptr;         // surrogate backend (mxb_demag_create_fno): no FFT plan
     cudaStream_t st = nullptr;
     cudaStream_t own = nullptr;
     uint64_t uid = ++g_demag_uid;   // identity for cached CUDA graphs
@@ -76,6 +81,11 @@ struct mxb_ctx {
     double* partials = nullptr;
     int last_nparts = 0;          // partials of the last mxb_stage_dev final stage
     bool state_valid = false;
+    // <m> of the resident state from the last committed step (the step commit
+    // reduces it anyway): serves the sample rows and the next run's previous
+    // mean without another pass over the state; cleared when the state changes
+    bool mean_ok = false;
+    double mean_c[3] = {0.0, 0.0, 0.0};
     // pinned bounce chunks for host copies to/from pageable memory
     char* bounce[2] = {nullptr, nullptr};
     cudaEvent_t bev[2] = {nullptr, nullptr};
@@ -226,6 +236,15 @@ int mxb_ctx_set_exact(mxb_ctx* c, int exact) {
 // ---------------------------------------------------------------------------
 // demag objects
 // ---------------------------------------------------------------------------
+// FFT-only entry points refuse a surrogate handle (mxb_demag_create_fno)
+static int fft_only(mxb_demag* d) {
+    if (d && d->fno) {
+        set_error("this is a surrogate demag handle: no FFT plan / spectra");
+        return MXB_EINVAL;
+    }
+    return MXB_OK;
+}
+
 int mxb_demag_create_slab(const mxb_grid* gr, int device, int nranks, int rank, mxb_demag** out) {
     int rc = check_grid(gr);
     if (rc) return rc;
@@ -244,6 +263,32 @@ int mxb_demag_create_slab(const mxb_grid* gr, int device, int nranks, int rank, 
 
 int mxb_demag_create(const mxb_grid* gr, int device, mxb_demag** out) {
     return mxb_demag_create_slab(gr, device, 1, 0, out);
+}
+
+int mxb_demag_create_fno(const mxb_grid* gr, int device, mxb_fno* f, mxb_demag** out) {
+    int rc = check_grid(gr);
+    if (rc) return rc;
+    if (!out || !f) { set_error("null argument"); return MXB_EINVAL; }
+    int H = 0, W = 0;
+    fno_forward_on(f, nullptr, nullptr, nullptr, &H, &W);
+    if (gr->nz != 1 || gr->ny != H || gr->nx != W) {
+        set_error("the surrogate backend needs a thin film (nz = 1) of the model's H x W");
+        return MXB_EINVAL;
+    }
+    mxb_demag* d = new mxb_demag();
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete d; return cuda_fail(e, "stream", __FILE__, __LINE__); }
+    d->own = d->st;
+    DemagPlan& p = d->plan;
+    p.dev = device;
+    p.g.nx = (int)gr->nx; p.g.ny = (int)gr->ny; p.g.nz = 1;
+    p.g.N = (long long)gr->nx * gr->ny;
+    p.g.dx = gr->dx; p.g.dy = gr->dy; p.g.dz = gr->dz;
+    p.has_kernel = true;
+    d->fno = f;
+    *out = d;
+    return MXB_OK;
 }
 
 int mxb_demag_destroy(mxb_demag* d) {
@@ -267,6 +312,7 @@ int mxb_demag_slab_info(mxb_demag* d, int64_t info[8]) {
 
 int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv) {
     if (!d || !send || !recv) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     *send = d->plan.XS;
     *recv = d->plan.XR;
     return MXB_OK;
@@ -274,24 +320,28 @@ int mxb_demag_slab_buffers(mxb_demag* d, void** send, void** recv) {
 
 int mxb_demag_slab_block(mxb_demag* d, int64_t* elems) {
     if (!d || !elems) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     *elems = d->plan.blk;
     return MXB_OK;
 }
 
 int mxb_demag_x_forward(mxb_demag* d, const double* m) {
     if (!d || !m) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     cudaSetDevice(d->plan.dev);
     return d->plan.x_forward(m, d->st, nullptr);
 }
 
 int mxb_demag_yz(mxb_demag* d) {
     if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     cudaSetDevice(d->plan.dev);
     return d->plan.yz(d->st, nullptr);
 }
 
 int mxb_demag_x_inverse(mxb_demag* d, double* h) {
     if (!d || !h) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     cudaSetDevice(d->plan.dev);
     return d->plan.x_inverse(h, d->st, nullptr);
 }
@@ -312,6 +362,7 @@ size_t mxb_demag_bytes(mxb_demag* d) { return d ? d->plan.bytes : 0; }
 
 int mxb_demag_set_packed(mxb_demag* d, const double* packed) {
     if (!d || !packed) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     DemagPlan& p = d->plan;
     cudaSetDevice(p.dev);
     const size_t n = (size_t)6 * p.pz * p.py * p.px;
@@ -329,6 +380,7 @@ int mxb_demag_set_packed(mxb_demag* d, const double* packed) {
 
 int mxb_demag_build(mxb_demag* d, int symmetric) {
     if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     DemagPlan& p = d->plan;
     cudaSetDevice(p.dev);
     const Grid& g = p.g;
@@ -357,6 +409,7 @@ int mxb_demag_build(mxb_demag* d, int symmetric) {
 
 int mxb_demag_tensor_elements(mxb_demag* d, double* out) {
     if (!d || !out) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     DemagPlan& p = d->plan;
     cudaSetDevice(p.dev);
     const Grid& g = p.g;
@@ -378,6 +431,7 @@ int mxb_demag_tensor_elements(mxb_demag* d, double* out) {
 
 int mxb_demag_direct(mxb_demag* d, const double* n6_host, const double* m_host, double* h_host) {
     if (!d || !m_host || !h_host) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     DemagPlan& p = d->plan;
     cudaSetDevice(p.dev);
     const Grid& g = p.g;
@@ -413,6 +467,7 @@ int mxb_demag_direct(mxb_demag* d, const double* n6_host, const double* m_host, 
 
 int mxb_demag_get_spectra(mxb_demag* d, double* out) {
     if (!d || !out) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     DemagPlan& p = d->plan;
     if (!p.has_kernel) { set_error("no spectra"); return MXB_EINVAL; }
     cudaSetDevice(p.dev);
@@ -509,6 +564,7 @@ int mxb_demag_kmode(mxb_demag* d, int* kmode) {
 
 int mxb_demag_set_fast(mxb_demag* d, int fast) {
     if (!d) { set_error("null argument"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     if (d->plan.pipe && !fast) {
         set_error("the plane pipeline has no generic path (build the kernel with MXB_PIPE=0)");
         return MXB_EINVAL;
@@ -524,6 +580,7 @@ int mxb_demag_set_fast(mxb_demag* d, int fast) {
 int mxb_demag_field_dev(mxb_demag* d, const double* m, double* h) {
     if (!d || !m || !h) { set_error("null argument"); return MXB_EINVAL; }
     cudaSetDevice(d->plan.dev);
+    if (d->fno) return fno_forward_on(d->fno, m, h, d->st, nullptr, nullptr);
     return d->plan.field_dev(m, h, d->st, nullptr);
 }
 
@@ -535,7 +592,8 @@ int mxb_demag_field(mxb_demag* d, const double* m, double* h) {
     int rc;
     if ((rc = ensure(&d->io[0], b)) || (rc = ensure(&d->io[1], b))) return rc;
     MXB_CUDA(cudaMemcpyAsync(d->io[0], m, b, cudaMemcpyHostToDevice, d->st));
-    rc = p.field_dev(d->io[0], d->io[1], d->st, nullptr);
+    rc = d->fno ? fno_forward_on(d->fno, d->io[0], d->io[1], d->st, nullptr, nullptr)
+                : p.field_dev(d->io[0], d->io[1], d->st, nullptr);
     if (rc) return rc;
     MXB_CUDA(cudaMemcpyAsync(h, d->io[1], b, cudaMemcpyDeviceToHost, d->st));
     MXB_CUDA(cudaStreamSynchronize(d->st));
@@ -575,6 +633,7 @@ static int download_out(mxb_ctx* c, double* h) {
 
 // demag (if enabled) into c->Hd, reading `m_dev` on the context stream
 static int demag_into(mxb_ctx* c, mxb_demag* d, const double* m_dev, double* hd, const int* halt) {
+    if (d->fno) return fno_forward_on(d->fno, m_dev, hd, c->st, nullptr, nullptr);
     return d->plan.field_dev(m_dev, hd, c->st, halt);
 }
 
@@ -831,8 +890,12 @@ int mxb_state_set(mxb_ctx* c, const double* m) {
     int rc = ensure_state(c);
     if (rc) return rc;
     c->cur = 0;
+    c->mean_ok = false;
     if ((rc = copy_to_device(c, c->Yb[0], m, fbytes(c->g)))) return rc;
     c->state_valid = true;
+    // the final readback of a large state goes through the bounce chunks:
+    // allocate them now rather than at the end of the run
+    if (fbytes(c->g) > kBounce && (rc = ensure_bounce(c))) return rc;
     return MXB_OK;
 }
 
@@ -844,6 +907,10 @@ int mxb_state_get(mxb_ctx* c, double* m) {
 
 int mxb_state_mean(mxb_ctx* c, double out[3]) {
     if (!c || !out || !c->state_valid) { set_error("no resident state"); return MXB_EINVAL; }
+    if (c->mean_ok) {
+        for (int q = 0; q < 3; ++q) out[q] = c->mean_c[q];
+        return MXB_OK;
+    }
     cudaSetDevice(c->dev);
     return mean_dev(c, c->Yb[c->cur], out);
 }
@@ -1048,7 +1115,12 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     if (ra->nsteps <= 0) return MXB_OK;
     // control block: previous mean = mean of the current state
     double prev[3] = {0, 0, 0};
-    if (c->n_magnetic > 0 && (rc = mean_dev(c, c->Yb[c->cur], prev))) return rc;
+    if (c->mean_ok) {
+        for (int q = 0; q < 3; ++q) prev[q] = c->mean_c[q];
+    } else if (c->n_magnetic > 0 && (rc = mean_dev(c, c->Yb[c->cur], prev))) {
+        return rc;
+    }
+    c->mean_ok = false;
     Ctl h{};
     h.dead_flat = LLONG_MAX;
     h.n_magnetic = c->n_magnetic > 0 ? c->n_magnetic : 1;
@@ -1142,6 +1214,11 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     st->drift = h.drift;
     st->dead_flat = h.dead_flat == LLONG_MAX ? -1 : h.dead_flat;
     st->status = h.halt;
+    if (h.halt == MXB_OK || h.halt == MXB_EQUILIBRATED) {
+        // h.mean: <m> of the committed state (or the previous mean if no step committed)
+        for (int q = 0; q < 3; ++q) c->mean_c[q] = h.mean[q];
+        c->mean_ok = c->n_magnetic > 0;
+    }
     if (h.halt == MXB_EBLOWUP) { set_error("integration blew up"); return MXB_EBLOWUP; }
     if (h.halt == MXB_EDEAD) { set_error("magnetic cell with |M| = 0"); return MXB_EDEAD; }
     if (h.halt == MXB_ECUDA) {
@@ -1227,6 +1304,7 @@ int mxb_ctl_get(mxb_ctx* c, mxb_run_stats* st) {
 // ---------------------------------------------------------------------------
 int mxb_time_demag(mxb_ctx* c, mxb_demag* d, int iters, double* ms_eval, double* ms_pass5) {
     if (!c || !d || !c->state_valid || iters < 1) { set_error("need ctx, demag and a resident state"); return MXB_EINVAL; }
+    if (fft_only(d)) return MXB_EINVAL;
     cudaSetDevice(c->dev);
     int rc = check_demag(c, d);
     if (rc) return rc;
@@ -1256,6 +1334,7 @@ int mxb_time_demag(mxb_ctx* c, mxb_demag* d, int iters, double* ms_eval, double*
 int mxb_time_steps(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, double dt, int nsteps,
                    const double bias[3], double* ms_total, double* ms_stencil, int64_t* launches) {
     if (!c || !t || !c->state_valid) { set_error("need ctx and a resident state"); return MXB_EINVAL; }
+    c->mean_ok = false;
     cudaSetDevice(c->dev);
     const bool use_demag = (t->mask & MXB_TERM_DEMAG) != 0;
     int rc;

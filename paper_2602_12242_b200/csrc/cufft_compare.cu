@@ -76,7 +76,7 @@ extern "C" int mxb_time_demag_cufft(mxb_demag* d, int iters, double* ms_eval) {
     if (!d || iters < 1) { set_error("bad argument"); return MXB_EINVAL; }
     DemagPlan& p = *demag_plan_of(d);
     cudaStream_t st = demag_stream_of(d);
-    if (!p.has_kernel) { set_error("no spectra"); return MXB_EINVAL; }
+    if (!p.has_kernel || !p.XS) { set_error("no spectra (or a surrogate handle)"); return MXB_EINVAL; }
     cudaSetDevice(p.dev);
     const Grid& g = p.g;
     const long long real_n = (long long)p.px * p.py * p.pz;

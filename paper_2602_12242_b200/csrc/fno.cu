@@ -317,6 +317,26 @@ void mxb_fno_destroy(mxb_fno* h) {
     delete h;
 }
 
+}  // extern "C"
+
+namespace mxb {
+// the forward pass on another stream (the solver's: the surrogate runs inside
+// the captured step of mxb_run, api.cu demag_into)
+int fno_forward_on(mxb_fno* h, const double* x, double* y, cudaStream_t st, int* H, int* W) {
+    if (!h) { set_error("null argument"); return MXB_EINVAL; }
+    if (H) *H = h->f.H;
+    if (W) *W = h->f.W;
+    if (!x || !y) return MXB_OK;
+    cudaStream_t own = h->f.st;
+    h->f.st = st;
+    const int rc = fno_forward(h->f, x, y);
+    h->f.st = own;
+    return rc;
+}
+}  // namespace mxb
+
+extern "C" {
+
 int mxb_fno_infer_dev(mxb_fno* h, const double* x, double* y) {
     if (!h || !x || !y) { set_error("null argument"); return MXB_EINVAL; }
     cudaSetDevice(h->f.dev);

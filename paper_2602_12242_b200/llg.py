@@ -111,8 +111,14 @@ class PartitionedRHS:
         self._demag_dev = None
         self._demag_fn = None
         if demag is not None:
+            dk = demag._device_kernel() if hasattr(demag, "_device_kernel") else None
             if isinstance(demag, DemagKernel):
                 self._demag_dev = demag
+                fn = demag.field
+            elif dk is not None:
+                # a plugin with a device evaluation (the FNO surrogate): evaluated
+                # inside the fused device step like the FFT kernel
+                self._demag_dev = dk
                 fn = demag.field
             else:
                 fn = demag.field if hasattr(demag, "field") else demag

@@ -266,3 +266,40 @@ def test_backend_wrappers_and_solver_plugin(tmp_path):
     small = mx.GridSpec(4, 4, 1, 3e-9, 3e-9, 3e-9)
     with pytest.raises(F.MagwError, match="spectral extent"):
         F.FnoDemag.load(p, mx.MaterialMap(small, Ms=8e5))
+
+
+@gpu
+def test_surrogate_runs_inside_the_device_loop(tmp_path):
+    """A loaded (frozen) FnoDemag is evaluated inside the fused device step
+    (mxb_demag_create_fno: the forward pass on the solver stream, captured in
+    the step graph) instead of from the host per stage; the trajectory equals
+    the host-orchestrated plug-in run (field() per stage, integrators.py)."""
+    from paper_2602_12242_b200.fno import _FnoKernel
+    grid = mx.GridSpec(32, 16, 1, 3e-9, 3e-9, 3e-9)
+    mat = mx.MaterialMap(grid, Ms=8e5, A=1.3e-11, alpha=0.1)
+    p = tmp_path / "m.magw"
+    t = small_tensors(seed=16)
+    write_model(p, t)
+    backend = F.FnoDemag.load(p, mat)
+    rhs = mx.PartitionedRHS(mat, exchange=True, demag=backend, bias=(2e4, 0.0, 0.0))
+    assert isinstance(rhs._demag_dev, _FnoKernel) and rhs._device_ok()
+    m0 = np.random.default_rng(7).standard_normal((3, 1, 16, 32))
+    m0 = mx.VectorField3(grid, m0)
+    mx.renormalize(m0, mat)
+    # device evaluation == the plug-in's host evaluation
+    assert np.max(np.abs(rhs.h_total_quiet(0.0, m0.data) - (
+        mx.exchange_field(m0, mat) + backend.field(m0.data) + np.array([2e4, 0, 0])[:, None, None, None]))) \
+        <= 1e-12 * 8e5
+    st = mx.SimState(m0.copy())
+    tr = mx.Simulation(st, rhs, mx.IntegratorSpec("rk4", 2e-14), sample_every=5,
+                       energy_in_samples=False).run_until(mx.StopCondition(max_steps=20))
+    # the host-orchestrated reference: the same backend through a plain callable (no device kernel)
+    rhs_h = mx.PartitionedRHS(mat, exchange=True, demag=lambda md: backend.field(md), bias=(2e4, 0.0, 0.0))
+    assert not rhs_h._device_ok()
+    st_h = mx.SimState(m0.copy())
+    tr_h = mx.Simulation(st_h, rhs_h, mx.IntegratorSpec("rk4", 2e-14), sample_every=5,
+                         energy_in_samples=False).run_until(mx.StopCondition(max_steps=20))
+    assert np.max(np.abs(st.m.data - st_h.m.data)) <= 1e-12 * 8e5
+    for k in ("mx", "my", "mz"):
+        assert np.max(np.abs(tr.column(k) - tr_h.column(k))) <= 1e-12
+    assert tr.counters["demag"] == tr_h.counters["demag"] == 80
