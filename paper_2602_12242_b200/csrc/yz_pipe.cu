@@ -73,6 +73,9 @@
 #ifndef MXB_PIPE_KPAIR_512  // the same in the L = 512 pair kernel (256^3: 16.28 -> 15.94 ms per step)
 #define MXB_PIPE_KPAIR_512 1
 #endif
+#ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
+#define MXB_PIPE_PF_NEXT 0
+#endif
 #ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too
 #define MXB_PIPE_HINT_K 0
 #endif
@@ -501,6 +504,18 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     double2* Wc = W + c * L;
     const Sched sc(a, L, halt);
     const TicketMap tmap{hx, N, L};
+#if MXB_PIPE_PF_NEXT
+    // thread 0, once the next ticket is known: an A unit's XP row comes from
+    // DRAM -- start pulling it into L2 while this unit finishes
+    auto prefetch_next_a = [&](long long t) {
+        const Unit nu = tmap(t);
+        if (nu.kind == U_A)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             a.XP + xp_row(a, plane_xp, nu.plane, nu.idx, N * 3)),
+                         "r"(3 * N * 16)
+                         : "memory");
+    };
+#endif
 
     auto stage = [&](const Unit& u) {
         double2* slot = a.slot + (long long)(u.plane % 3) * slot_e;
@@ -686,7 +701,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         bool inverse = cur.kind == U_C;
         if (cur.kind != U_C) {
             fw::fft1024<-1, MXB_HALF_IN != 0>(v, Wc, lane, tw);
-            if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+            if (threadIdx.x == 0) {
+                next_ticket = atomicAdd(sc.ticket(), 1u);
+#if MXB_PIPE_PF_NEXT
+                prefetch_next_a(next_ticket);
+#endif
+            }
             if (cur.kind == U_A) {
                 // ---- y forward of row z = idx -> slot row [ky][c]
 #if MXB_PIPE_W_DIRECT_STORE
@@ -779,7 +799,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             fw::fft1024<1>(v, Wc, lane, tw);
             if (cur.kind == U_C) {
                 // ---- y inverse of row z = idx -> XP row (n of L kept)
-                if (threadIdx.x == 0) next_ticket = atomicAdd(sc.ticket(), 1u);
+                if (threadIdx.x == 0) {
+                    next_ticket = atomicAdd(sc.ticket(), 1u);
+#if MXB_PIPE_PF_NEXT
+                    prefetch_next_a(next_ticket);
+#endif
+                }
 #if MXB_PIPE_W_DIRECT_STORE
                 double2* dst = a.XP + xp_row(a, plane_xp, cur.plane, cur.idx, N * 3) + c;
 #pragma unroll
