@@ -76,8 +76,8 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
-#ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too
-#define MXB_PIPE_HINT_K 0
+#ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too: same kernel time,
+#define MXB_PIPE_HINT_K 1   // 27.7 instead of 36.9 GB of DRAM per launch -> more clock under the power cap
 #endif
 #if MXB_PIPE_HINTS
 #define PIPE_POL_STREAM() policy_evict_first()
