@@ -73,6 +73,9 @@
 #ifndef MXB_PIPE_KPAIR_512  // the same in the L = 512 pair kernel (256^3: 16.28 -> 15.94 ms per step)
 #define MXB_PIPE_KPAIR_512 1
 #endif
+#ifndef MXB_PIPE_EARLY_READY // read the next unit's dependency counter during the current unit
+#define MXB_PIPE_EARLY_READY 0
+#endif
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
@@ -139,6 +142,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -256,12 +265,20 @@ struct Sched {
     // CTA-wide wait for u's inputs.  Never blocks while holding an unsignalled
     // unit (deferred signals could otherwise form a cycle between CTAs);
     // pending is thread 0's.  Returns false on abort.
-    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending) const {
+    // early: thread 0's relaxed read of u's counter, issued during the previous
+    // unit (MXB_PIPE_EARLY_READY); if it already shows the target, the acquire
+    // is a fence instead of another L2 round trip on the critical path
+    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending, unsigned early = 0u) const {
         if (threadIdx.x == 0) {
             *flag = 1;
             const unsigned* c;
             unsigned tg;
-            if (dep(u, &c, &tg) && ld_acquire(c) < tg) {
+            bool need = dep(u, &c, &tg);
+            if (need && early >= tg) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                need = false;
+            }
+            if (need && ld_acquire(c) < tg) {
                 if (pending.kind != U_NONE) {
                     // the pending unit's bulk / TMA stores (async proxy) must have
                     // completed, not only read shared memory, before consumers see
@@ -504,6 +521,15 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     double2* Wc = W + c * L;
     const Sched sc(a, L, halt);
     const TicketMap tmap{hx, N, L};
+#if MXB_PIPE_EARLY_READY
+    unsigned early = 0u;   // thread 0: the next unit's dependency counter, read during this unit
+    auto early_read = [&](long long t) -> unsigned {
+        const Unit nu = tmap(t);
+        const unsigned* cc;
+        unsigned tg;
+        return sc.dep(nu, &cc, &tg) ? ld_relaxed(cc) : 0u;
+    };
+#endif
 #if MXB_PIPE_PF_NEXT
     // thread 0, once the next ticket is known: an A unit's XP row comes from
     // DRAM -- start pulling it into L2 while this unit finishes
@@ -663,7 +689,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     Unit pending{U_NONE, 0, 0};
 
     while (cur.kind != U_NONE) {
+#if MXB_PIPE_EARLY_READY
+        if (!sc.wait_ready(cur, &flag, pending, early)) return;
+        early = 0u;
+#else
         if (!sc.wait_ready(cur, &flag, pending)) return;
+#endif
         stage(cur);
         stage_wait(cur);
         if (pending.kind != U_NONE) {
@@ -705,6 +736,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                 next_ticket = atomicAdd(sc.ticket(), 1u);
 #if MXB_PIPE_PF_NEXT
                 prefetch_next_a(next_ticket);
+#endif
+#if MXB_PIPE_EARLY_READY
+                early = early_read(next_ticket);
 #endif
             }
             if (cur.kind == U_A) {
@@ -803,6 +837,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
                     next_ticket = atomicAdd(sc.ticket(), 1u);
 #if MXB_PIPE_PF_NEXT
                     prefetch_next_a(next_ticket);
+#endif
+#if MXB_PIPE_EARLY_READY
+                    early = early_read(next_ticket);
 #endif
                 }
 #if MXB_PIPE_W_DIRECT_STORE
