@@ -73,6 +73,12 @@
 #ifndef MXB_PIPE_KPAIR_512  // the same in the L = 512 pair kernel (256^3: 16.28 -> 15.94 ms per step)
 #define MXB_PIPE_KPAIR_512 1
 #endif
+#ifndef MXB_PIPE_DISCARD_LATE   // C units drop their slot row after the inverse FFT, not before
+#define MXB_PIPE_DISCARD_LATE 0
+#endif
+#ifndef MXB_PIPE_SIGNAL_REL     // completion signals as red.release instead of fence + atomicAdd
+#define MXB_PIPE_SIGNAL_REL 0
+#endif
 #ifndef MXB_PIPE_EARLY_READY // read the next unit's dependency counter during the current unit
 #define MXB_PIPE_EARLY_READY 0
 #endif
@@ -258,8 +264,13 @@ struct Sched {
     // after a __syncthreads that follows the unit's stores; thread 0
     __device__ void signal(const Unit& u) const {
         if (threadIdx.x == 0) {
+#if MXB_PIPE_SIGNAL_REL
+            // one release reduction instead of a full fence and a relaxed atomic
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done_of(u)) : "memory");
+#else
             __threadfence();
             atomicAdd(const_cast<unsigned*>(done_of(u)), 1u);
+#endif
         }
     }
     // CTA-wide wait for u's inputs.  Never blocks while holding an unsignalled
@@ -708,7 +719,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         }
         __syncthreads();
         double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
-#if MXB_PIPE_DISCARD
+#if MXB_PIPE_DISCARD && !MXB_PIPE_DISCARD_LATE
         if (cur.kind == U_C) {
             // the slot row is dead until A(p+3, z) rewrites it: drop its L2 lines
             // without writing them back (48 KB = 384 lines of 128 B)
@@ -831,6 +842,13 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         }
         if (inverse) {
             fw::fft1024<1>(v, Wc, lane, tw);
+#if MXB_PIPE_DISCARD && MXB_PIPE_DISCARD_LATE
+            if (cur.kind == U_C) {
+                char* row = reinterpret_cast<char*>(slot + (long long)cur.idx * L * 3);
+                for (int j = threadIdx.x; j < 3 * L * 16 / 128; j += 96)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(row + (size_t)j * 128) : "memory");
+            }
+#endif
             if (cur.kind == U_C) {
                 // ---- y inverse of row z = idx -> XP row (n of L kept)
                 if (threadIdx.x == 0) {
