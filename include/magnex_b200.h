@@ -252,6 +252,10 @@ typedef struct mxb_stage_io {
 /* mode: 0 H_eff, 1 dM/dt, 2-5 RK4 stages 1-4, 6 Euler.  Modes 5/6 leave block
  * partials for mxb_step_partials_dev instead of committing the step. */
 int mxb_stage_dev(mxb_ctx* ctx, int mode, const mxb_terms* t, const mxb_stage_io* io);
+/* z-slab halos: copy the first and last local z planes of the three
+ * components of f (3,nz,ny,nx, device) into the contiguous send buffers
+ * lo/hi (3,ny,nx each) with one kernel on the context stream */
+int mxb_pack_halo_planes(mxb_ctx* ctx, const double* f, double* lo, double* hi);
 /* out8 = {sum mx/Ms, sum my/Ms, sum mz/Ms, 0 | max drift, halt code, -dead_flat, 0}
  * (first four summed over ranks, last four max-reduced over ranks by the caller) */
 int mxb_step_partials_dev(mxb_ctx* ctx, double* out8_dev);

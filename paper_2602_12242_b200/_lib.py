@@ -111,6 +111,7 @@ SIGNATURES = {
     "mxb_demag_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
     "mxb_ctx_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
     "mxb_stage_dev": ([C.c_void_p, C.c_int, C.POINTER(Terms), C.POINTER(StageIO)], C.c_int),
+    "mxb_pack_halo_planes": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "mxb_step_partials_dev": ([C.c_void_p, C.c_void_p], C.c_int),
     "mxb_step_commit_dev": ([C.c_void_p, C.c_void_p], C.c_int),
     "mxb_ctl_reset": ([C.c_void_p, _dp, C.c_int64, C.c_double], C.c_int),

@@ -1255,6 +1255,28 @@ int mxb_stage_dev(mxb_ctx* c, int mode, const mxb_terms* t, const mxb_stage_io* 
     return launch_stage(mode, c->exact, a, c->st, false);
 }
 
+__global__ void k_pack_halo(const double* __restrict__ f, double* __restrict__ lo, double* __restrict__ hi,
+                            long long plane, long long N, int nz) {
+    const long long tot = 3 * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / plane, p = i - c * plane;
+        lo[i] = f[c * N + p];
+        hi[i] = f[c * N + (long long)(nz - 1) * plane + p];
+    }
+}
+
+int mxb_pack_halo_planes(mxb_ctx* c, const double* f, double* lo, double* hi) {
+    if (!c || !f || !lo || !hi) { set_error("null argument"); return MXB_EINVAL; }
+    cudaSetDevice(c->dev);
+    const long long plane = (long long)c->g.nx * c->g.ny;
+    const long long tot = 3 * plane;
+    const unsigned nb = (unsigned)std::min<long long>((tot + 255) / 256, 148LL * 8);
+    k_pack_halo<<<nb, 256, 0, c->st>>>(f, lo, hi, plane, c->g.N, c->g.nz);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
+}
+
 int mxb_step_partials_dev(mxb_ctx* c, double* out8) {
     if (!c || !out8) { set_error("null argument"); return MXB_EINVAL; }
     cudaSetDevice(c->dev);

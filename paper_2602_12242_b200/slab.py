@@ -195,9 +195,10 @@ class CudaSlabBackend:
         return self.fields[name].cpu().numpy()
 
     def boundary_planes(self, name):
-        f = self.fields[name]
-        self.halo["send_lo"].copy_(f[:, 0])
-        self.halo["send_hi"].copy_(f[:, -1])
+        # both boundary planes of the three components in one kernel (mxb_pack_halo_planes)
+        L.check(self.ctx.call("mxb_pack_halo_planes", C.c_void_p(self.fields[name].data_ptr()),
+                              C.c_void_p(self.halo["send_lo"].data_ptr()),
+                              C.c_void_p(self.halo["send_hi"].data_ptr())), "pack_halo")
         return self.halo["send_lo"], self.halo["send_hi"], self.halo["lo"], self.halo["hi"]
 
     def material_halos(self, comm, lo_rank, hi_rank):
