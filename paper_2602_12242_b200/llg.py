@@ -23,7 +23,7 @@ from .demag import DemagKernel
 from .fields import (AnisotropyOperator, BulkDmiOperator, CubicAnisotropyOperator, DmiOperator,
                      EnergyBreakdown, ExchangeOperator, _StencilPlan)
 from .grid import MaterialMap, RenormalizeError, VectorField3, _raise_dead, mean_normalized, renormalize
-from .integrators import (_MRI_DC, KW3_C, euler_step, fast_evals_per_step, mri_kw3_step, rk4_step,
+from .integrators import (_PHASE_WIDTH, KW3_C, euler_step, fast_evals_per_step, mri_kw3_step, rk4_step,
                           substeps_per_phase)
 
 __all__ = ["SLOW_EXPLICIT", "FAST", "SLOW_IMPLICIT", "TERMS", "llg_rhs", "PartitionedRHS",
@@ -416,7 +416,7 @@ class Simulation:
         times = [t] if slow else []
         for ph in range(3):
             if not slow:
-                span = _MRI_DC[ph] * dt
+                span = _PHASE_WIDTH[ph] * dt
                 t0 = t + KW3_C[ph] * dt
                 h = span / nsub[ph]
                 for s in range(nsub[ph]):
