@@ -186,3 +186,29 @@ def test_direct_sum_guard():
     g = mx.GridSpec(17, 17, 17, 1e-9, 1e-9, 1e-9)
     with pytest.raises(ValueError, match="direct sum limited"):
         mx.demag_field_direct(mx.VectorField3(g, np.zeros((3,) + g.shape)), g)
+
+
+def test_host_integrators_match_oracle():
+    """The array-level steppers (used for plug-in right-hand sides) keep the
+    reference's floating-point association: bit-identical to the oracle's
+    restatement (itself pinned bit-exactly to reference traces)."""
+    from paper_2602_12242_b200 import integrators as I
+    rng = np.random.default_rng(0)
+    y = rng.normal(size=(3, 4, 5))
+    A = rng.normal(size=(3, 3))
+
+    def f(t, v):
+        return np.tanh(np.einsum("ij,j...->i...", A, v)) * (1 + t)
+
+    def g(t, v):
+        return -0.3 * v + 0.1 * t
+
+    def post(v):
+        return v / np.sqrt((v * v).sum(0, keepdims=True))
+
+    assert np.array_equal(I.euler_step(y, 0.1, 0.01, f), O.euler_step(y, 0.1, 0.01, f))
+    assert np.array_equal(I.rk4_step(y, 0.1, 0.01, f, post), O.rk4_step(y, 0.1, 0.01, f, post))
+    assert np.array_equal(I.kw3_step(y, 0.1, 0.01, f, post), O.kw3_step(y, 0.1, 0.01, f, post))
+    assert np.array_equal(I.mri_kw3_step(y, 0.1, 0.01, f, g, 0.15, post),
+                          O.mri_kw3_step(y, 0.1, 0.01, f, g, 0.15, post))
+    assert I.substeps_per_phase(0.1) == (4, 5, 3) and I.fast_evals_per_step(0.1) == 36
