@@ -402,6 +402,8 @@ void DemagPlan::release() {
     bar = nullptr;
     if (Kc && Kc != K) cudaFree(Kc);
     if (K) cudaFree(K);
+    if (T) cudaFree(T);
+    T = nullptr;
     if (X2 && X2 != XR) cudaFree(X2);
     if (XR && XR != XS) cudaFree(XR);
     if (XS) cudaFree(XS);
@@ -410,12 +412,31 @@ void DemagPlan::release() {
     twm = nullptr;
 }
 
+// The spectra are built per rank: one rank keeps all hx planes; a slab rank
+// (G > 1) transforms each component along x into a one-component scratch T and
+// keeps only its kx chunk, so the y/z transforms and the build memory scale
+// with hx/G (the 2048^2 x 64 film: ~17 + 13 GB per rank instead of 103 GB).
 static int alloc_full_spectra(DemagPlan& p, cudaStream_t st) {
     if (p.K) return MXB_OK;
-    const size_t n = (size_t)p.pz * p.py * p.hxp * 6;
+    p.kpitch = p.G > 1 ? p.CHP : p.hxp;
+    p.koff = p.G > 1 ? p.kx0 : 0;
+    const size_t n = (size_t)p.pz * p.py * p.kpitch * 6;
     MXB_CUDA(cudaMalloc(&p.K, n * sizeof(double2)));
     MXB_CUDA(cudaMemsetAsync(p.K, 0, n * sizeof(double2), st));
+    if (p.G > 1 && !p.T) MXB_CUDA(cudaMalloc(&p.T, (size_t)p.pz * p.py * p.hxp * sizeof(double2)));
     return MXB_OK;
+}
+
+// one component's kx chunk [kx0, kx0 + kxn) of the full x spectrum into slot c of K
+__global__ void k_take_chunk(const double2* __restrict__ T, double2* __restrict__ K, long long nzy, int hxp,
+                             int kx0, int kxn, int kpitch, int c) {
+    const long long tot = nzy * kpitch;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int kx = (int)(t % kpitch);
+        const long long zy = t / kpitch;
+        K[t * 6 + c] = kx < kxn ? T[zy * hxp + kx0 + kx] : make_double2(0.0, 0.0);
+    }
 }
 
 // x r2c of one packed real-space component (pz,py,px) into slot c of K
@@ -423,21 +444,27 @@ int DemagPlan::spectra_x_component(const double* Pc, int c, cudaStream_t st) {
     int rc = alloc_full_spectra(*this, st);
     if (rc) return rc;
     const long long plane = (long long)pz * py;
-    return launch_rows_r2c(plx, Pc, 0, px, px, K, hxp, hx, 1, plane, st, nullptr, 6, c);
+    if (G == 1) return launch_rows_r2c(plx, Pc, 0, px, px, K, hxp, hx, 1, plane, st, nullptr, 6, c);
+    if ((rc = launch_rows_r2c(plx, Pc, 0, px, px, T, hxp, hx, 1, plane, st, nullptr, 1, 0))) return rc;
+    k_take_chunk<<<148 * 8, 256, 0, st>>>(T, K, plane, hxp, kx0, kxn, kpitch, c);
+    MXB_LAUNCH_CHECK();
+    return MXB_OK;
 }
 
 // y and z forward transforms of all 6 slots of K, in place
 int DemagPlan::spectra_yz(cudaStream_t st) {
     int rc;
+    const int kp = kpitch;
     if (py > 1) {
-        // y lines: element stride hxp*6, Q = hxp*6 per z-plane
-        rc = launch_lines(-1, ply, K, K, py, py, (long long)hxp * 6, (long long)hxp * 6, hxp * 6,
-                          (long long)pz * hxp * 6, (long long)py * hxp * 6, (long long)py * hxp * 6,
+        // y lines: element stride kp*6, Q = kp*6 per z-plane
+        rc = launch_lines(-1, ply, K, K, py, py, (long long)kp * 6, (long long)kp * 6, kp * 6,
+                          (long long)pz * kp * 6, (long long)py * kp * 6, (long long)py * kp * 6,
                           st, nullptr);
         if (rc) return rc;
     }
+    if (T) { cudaFree(T); T = nullptr; }
     if (pz > 1) {
-        long long Q = (long long)py * hxp * 6;
+        long long Q = (long long)py * kp * 6;
         rc = launch_lines(-1, plz, K, K, pz, pz, Q, Q, (int)Q, Q, 0, 0, st, nullptr);
         if (rc) return rc;
     }
@@ -522,8 +549,8 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         MXB_CUDA(cudaMalloc(&bar, (2 + 3 * (size_t)hx + 3 * (size_t)g.nz) * sizeof(unsigned)));
         int rc = MXB_OK;
         if (kxn > 0)
-            rc = symmetric ? pipe_quarter(K, Kp, pz, kxn, hxp, st, kx0)
-                           : pipe_complex(K, reinterpret_cast<double2*>(Kp), pz, kxn, hxp, st, kx0);
+            rc = symmetric ? pipe_quarter(K, Kp, pz, kxn, kpitch, st, kx0 - koff)
+                           : pipe_complex(K, reinterpret_cast<double2*>(Kp), pz, kxn, kpitch, st, kx0 - koff);
         if (rc) return rc;
         CH = 1;
         CHP = 1;
@@ -572,15 +599,15 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         const int e_is_z = pz > 1 ? 1 : (py > 1 ? 0 : 1);
         const size_t n = (size_t)(L / 2 + 1) * (GG / 2 + 1) * CHP * 6;
         MXB_CUDA(cudaMalloc(&Kq, n * sizeof(double)));
-        k_quarterize<<<148 * 8, 256, 0, st>>>(K, Kq, L, GG, py, hxp, e_is_z, kx0, kxn, CHP);
+        k_quarterize<<<148 * 8, 256, 0, st>>>(K, Kq, L, GG, py, kpitch, e_is_z, kx0 - koff, kxn, CHP);
         MXB_LAUNCH_CHECK();
         kmode = 2;
-    } else if (G == 1) {
-        Kc = K;   // the chunk is the whole spectrum
+    } else if (G == 1 || (kpitch == CHP && koff == kx0)) {
+        Kc = K;   // the chunk is the whole (rank-built) spectrum
     } else {
         const size_t n = (size_t)pz * py * CHP * 6;
         MXB_CUDA(cudaMalloc(&Kc, n * sizeof(double2)));
-        k_chunk_complex<<<148 * 8, 256, 0, st>>>(K, Kc, (long long)pz * py, hxp, kx0, kxn, CHP);
+        k_chunk_complex<<<148 * 8, 256, 0, st>>>(K, Kc, (long long)pz * py, kpitch, kx0 - koff, kxn, CHP);
         MXB_LAUNCH_CHECK();
     }
     MXB_CUDA(cudaStreamSynchronize(st));

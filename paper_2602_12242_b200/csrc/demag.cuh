@@ -65,7 +65,10 @@ struct DemagPlan {
     double2* XS = nullptr;   // x-pass side, [G][nz_l][ny][CHP][3] (send layout)
     double2* XR = nullptr;   // kx-chunk side, [nz][ny][CHP][3] (== XS for one rank)
     double2* X2 = nullptr;   // [nz][py][CHP][3]
-    double2* K = nullptr;    // full spectra [pz][py][hxp][6] complex (build scratch)
+    double2* K = nullptr;    // spectra build scratch [pz][py][kpitch][6] complex: all hx planes
+                             // (one rank) or only this rank's kx chunk (slab: kpitch = CHP)
+    int kpitch = 0, koff = 0;   // kx pitch of K and the global kx of its first column
+    double2* T = nullptr;    // slab build: one component's full x spectrum [pz][py][hxp]
     double2* Kc = nullptr;   // complex spectra of the chunk [pz][py][CHP][6]
     double* Kq = nullptr;    // parity-reduced real spectra of the chunk [L/2+1][G/2+1][CHP][6]
     int kmode = 0;           // 0 complex Kc, 2 real quarter Kq, 3 plane pipeline Kp, 4 long-y Kp,
