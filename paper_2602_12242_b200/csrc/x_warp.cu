@@ -30,6 +30,10 @@ using namespace ff;
 #define MXB_XW_EXIT_READ 1
 #endif
 
+#ifndef MXB_XW_TWPRE   // c2r: untangling twiddles loaded before the TMA wait
+#define MXB_XW_TWPRE 0
+#endif
+
 namespace {
 constexpr int XM = 512;          // complex FFT length (px / 2)
 constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
@@ -166,12 +170,23 @@ k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restri
         }
     }
     __syncthreads();   // mbarrier initialised before anyone polls it
+#if MXB_XW_TWPRE
+    // the untangling twiddles do not depend on the spectra: load them while the
+    // TMA boxes are in flight
+    double2 twp[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) twp[m] = __ldg(tw1024 + lane + 32 * m);
+#endif
     mbar_wait(&mbar, 0);
     double2 a[16], b[16], v[32];
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
         const int k = lane + 32 * m;
+#if MXB_XW_TWPRE
+        const double2 w = twp[m];
+#else
         const double2 w = tw1024[k];
+#endif
 #pragma unroll
         for (int ln = 0; ln < 2; ++ln) {
             const double2 xk = S[PM ? (k * 2 + ln) * 3 + c : (ln * XHX + k) * 3 + c];
