@@ -16,6 +16,9 @@
 #ifndef MXB_HALF_IN
 #define MXB_HALF_IN 1   // zero-padded forward inputs skip the zero half of the first stage
 #endif
+#ifndef MXB_FFT_TW2
+#define MXB_FFT_TW2 0   // two interleaved twiddle chains in fft1024 (A/B)
+#endif
 
 #include "fft_fast.cuh"
 #include "fft_generic.cuh"
@@ -121,6 +124,27 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_i
     // w1024^(lane k) as a running product, re-anchored from the exact table
     // every 8 steps (<= 7 products; loading all 31 would pin ~120 registers)
     const double2 w1 = twid<DIR>(tw, lane);
+#if MXB_FFT_TW2
+    // two interleaved running products (k and k + 16), each re-anchored from the
+    // exact table every 8 steps: half the serial twiddle chain
+    double2 wa = make_double2(1.0, 0.0), wb = twid<DIR>(tw, lane * 16);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k & 7) {
+            wa = k == 1 ? w1 : cmul(wa, w1);
+            wb = cmul(wb, w1);
+        } else if (k) {
+            wa = twid<DIR>(tw, lane * k);
+            wb = twid<DIR>(tw, lane * (k + 16));
+        }
+        const double2 a = k ? cmul(v[p32(k)], wa) : v[p32(k)];
+        const double2 b = cmul(v[p32(k + 16)], wb);
+        W[tsw(k, lane)] = a;
+        W[tsw(k + 16, lane)] = b;
+        wa.x = fma(0.0, a.x, wa.x);
+        wb.x = fma(0.0, b.x, wb.x);
+    }
+#else
     double2 w = make_double2(1.0, 0.0);
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -133,6 +157,7 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2* W, int lane_i
         // twiddles would stay live across the first DFT
         w.x = fma(0.0, a.x, w.x);
     }
+#endif
     __syncwarp();
 #pragma unroll
     for (int l = 0; l < 32; ++l) v[l] = W[tsw(lane, l)];
