@@ -30,8 +30,8 @@ using namespace ff;
 #define MXB_XW_EXIT_READ 1
 #endif
 
-#ifndef MXB_XW_TWPRE   // c2r: untangling twiddles loaded before the TMA wait
-#define MXB_XW_TWPRE 0
+#ifndef MXB_XW_TWPRE   // c2r: untangling twiddles loaded before the TMA wait (6.89 -> 6.81 ms per step)
+#define MXB_XW_TWPRE 1
 #endif
 
 namespace {
