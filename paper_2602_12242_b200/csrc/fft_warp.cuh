@@ -20,10 +20,10 @@
 #define MXB_FFT_TW2 1   // two interleaved twiddle chains in fft1024: pipeline 80.8 -> 79.3 ms per step
 #endif
 #ifndef MXB_FFT_TW4
-#define MXB_FFT_TW4 0   // four interleaved chains (one per 8-block), A/B
+#define MXB_FFT_TW4 1   // four interleaved chains (one per 8-block): another -0.3%, no spills
 #endif
 #ifndef MXB_FFT512_TW2
-#define MXB_FFT512_TW2 0   // fft512x2: chains k and k + 8 interleaved, A/B
+#define MXB_FFT512_TW2 1   // fft512x2: chains k and k + 8 interleaved (x passes -0.8%)
 #endif
 
 #include "fft_fast.cuh"
