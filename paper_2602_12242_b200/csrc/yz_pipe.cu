@@ -85,6 +85,9 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
+#ifndef MXB_PIPE_KUNROLL    // unroll of the B multiply's kernel-entry loop (loads of the next entry in flight)
+#define MXB_PIPE_KUNROLL 1
+#endif
 #ifndef MXB_PIPE_HINT_K     // kernel-row loads with the evict_first hint too: same kernel time,
 #define MXB_PIPE_HINT_K 1   // 27.7 instead of 36.9 GB of DRAM per launch -> more clock under the power cap
 #endif
@@ -101,6 +104,8 @@
 namespace mxb {
 
 using namespace ff;
+
+constexpr int kKUnroll = MXB_PIPE_KUNROLL;
 
 struct PipeArgs {
     double2* XP;          // [hx][nz][ny][3], input and output (in place)
@@ -783,6 +788,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #if MXB_PIPE_KPAIR
                 // kz and L - kz share the parity-reduced entry kz' = min(kz, L - kz):
                 // each entry is loaded once and applied to both (sign flip of XZ, YZ)
+#if MXB_PIPE_KUNROLL > 1
+#pragma unroll(kKUnroll)
+#endif
                 for (int q = a.cplx ? L : threadIdx.x; q <= L / 2; q += 96) {
                     const double2* kr = krow + q * 3;
 #if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
