@@ -85,6 +85,9 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
+#ifndef MXB_PIPE_SEEN       // skip re-acquiring a plane counter this CTA already saw complete
+#define MXB_PIPE_SEEN 0
+#endif
 #ifndef MXB_PIPE_KUNROLL    // unroll of the B multiply's kernel-entry loop (loads of the next entry in flight)
 #define MXB_PIPE_KUNROLL 1
 #endif
@@ -284,16 +287,25 @@ struct Sched {
     // early: thread 0's relaxed read of u's counter, issued during the previous
     // unit (MXB_PIPE_EARLY_READY); if it already shows the target, the acquire
     // is a fence instead of another L2 round trip on the critical path
-    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending, unsigned early = 0u) const {
+    // seen (thread 0, optional): the last plane whose A units (seen[0]) / B units
+    // (seen[1]) this CTA has already observed complete with an acquire -- the
+    // per-plane counters only grow and that acquire already ordered this CTA's
+    // later reads after every producer, so further B / C units of the same
+    // plane skip the load
+    __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending, unsigned early = 0u,
+                               int* seen = nullptr) const {
         if (threadIdx.x == 0) {
             *flag = 1;
             const unsigned* c;
             unsigned tg;
             bool need = dep(u, &c, &tg);
+            if (need && seen && ((u.kind == U_B && seen[0] == u.plane) || (u.kind == U_C && seen[1] == u.plane)))
+                need = false;
             if (need && early >= tg) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 need = false;
             }
+            const bool observed = need;   // this unit's counter is read with an acquire below
             if (need && ld_acquire(c) < tg) {
                 if (pending.kind != U_NONE) {
                     // the pending unit's bulk / TMA stores (async proxy) must have
@@ -319,6 +331,10 @@ struct Sched {
                         break;
                     }
                 }
+            }
+            if (observed && seen && *flag) {
+                if (u.kind == U_B) seen[0] = u.plane;
+                if (u.kind == U_C) seen[1] = u.plane;
             }
         }
         __syncthreads();
@@ -537,6 +553,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     double2* Wc = W + c * L;
     const Sched sc(a, L, halt);
     const TicketMap tmap{hx, N, L};
+#if MXB_PIPE_SEEN
+    int seen[2] = {-1, -1};   // thread 0: planes whose A / B units are known complete
+#endif
 #if MXB_PIPE_EARLY_READY
     unsigned early = 0u;   // thread 0: the next unit's dependency counter, read during this unit
     auto early_read = [&](long long t) -> unsigned {
@@ -708,6 +727,8 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #if MXB_PIPE_EARLY_READY
         if (!sc.wait_ready(cur, &flag, pending, early)) return;
         early = 0u;
+#elif MXB_PIPE_SEEN
+        if (!sc.wait_ready(cur, &flag, pending, 0u, seen)) return;
 #else
         if (!sc.wait_ready(cur, &flag, pending)) return;
 #endif
