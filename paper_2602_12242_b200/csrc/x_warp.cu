@@ -30,6 +30,10 @@ using namespace ff;
 #define MXB_XW_EXIT_READ 1
 #endif
 
+#ifndef MXB_XW_TWREC   // r2c: untangling twiddles by products of W^32 between table anchors
+#define MXB_XW_TWREC 0
+#endif
+
 #ifndef MXB_XW_TWPRE   // c2r: untangling twiddles loaded before the TMA wait (6.89 -> 6.81 ms per step)
 #define MXB_XW_TWPRE 1
 #endif
@@ -95,10 +99,20 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
     // untangle all XHX bins of both lines into registers (bin kx = lane + 32 i)
     constexpr int NI = (XHX + 31) / 32;   // 17
     double2 xo[2][NI];
+#if MXB_XW_TWREC
+    // W^kx for kx = lane + 32 i: table anchors every 4th i, products with the exact
+    // W^32 in between (5 + 1 loads per lane instead of 17)
+    const double2 w32 = tw1024[32];
+    double2 wk = tw1024[lane];
+#endif
 #pragma unroll
-    for (int ln = 0; ln < 2; ++ln)
+    for (int i = 0; i < NI; ++i) {
+#if MXB_XW_TWREC
+        if (i % 4 == 0) { if (i) wk = tw1024[lane + 32 * i]; }
+        else wk = cmul(wk, w32);
+#endif
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
+        for (int ln = 0; ln < 2; ++ln) {
             const int kx = lane + 32 * i;
             if (kx < XHX) {
                 const double2 zk = Wc[ln * XM + (kx & (XM - 1))];
@@ -106,9 +120,14 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
                 // E = (Zk + conj Zm)/2, O = (Zk - conj Zm)/(2i), X = E + W^k O
                 const double2 E = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
                 const double2 Od = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+#if MXB_XW_TWREC
+                xo[ln][i] = cadd(E, cmul(wk, Od));
+#else
                 xo[ln][i] = cadd(E, cmul(tw1024[kx], Od));
+#endif
             }
         }
+    }
     __syncthreads();   // every warp is done with its tile: stage the output pair
 #pragma unroll
     for (int ln = 0; ln < 2; ++ln)
