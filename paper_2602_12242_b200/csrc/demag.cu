@@ -382,7 +382,8 @@ bool DemagPlan::pipe_candidate(bool symmetric) const {
 // film): plane-major spectra, row kernels for y, the fused z pass over
 // ky-contiguous chunks.  MXB_LONGY=0 keeps the 5-pass column kernels.
 bool DemagPlan::longy_candidate() const {
-    if (G != 1 || pz <= 1 || !fast || pipe) return false;
+    if (pz <= 1 || !fast || pipe) return false;
+    if (G > 1 && (nz_l < 1 || (nz_l & (nz_l - 1)))) return false;
     if (px < 4 || (px & (px - 1)) || (g.nx % 2)) return false;
     if (!longy_shape_ok(py) || !fast_fused_ok(pz)) return false;
     const char* e = getenv("MXB_LONGY");
@@ -568,9 +569,13 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
     if (symmetric && longy_candidate()) {
         // plane-major XR [kx][z][y][3] and X2 [kx][z][ky][3] (both fit the
         // row-major allocations), kernel Kp[kx][ky'][kz'][6]
-        const size_t nk = (size_t)hx * (py / 2 + 1) * (pz / 2 + 1) * 6;
+        // (on a z slab: the rank's kx chunk of CHr planes, XR the all-to-all receive blocks)
+        const int CHr = G == 1 ? hx : (hx + G - 1) / G;
+        kx0 = rank * CHr;
+        kxn = std::max(0, std::min(CHr, hx - kx0));
+        const size_t nk = (size_t)std::max(kxn, 1) * (py / 2 + 1) * (pz / 2 + 1) * 6;
         MXB_CUDA(cudaMalloc(&Kp, nk * sizeof(double)));
-        int rc = longy_quarter(K, Kp, py, pz, hx, hxp, st);
+        int rc = kxn > 0 ? longy_quarter(K, Kp, py, pz, kxn, kpitch, st, kx0 - koff) : MXB_OK;
         if (rc) return rc;
         if (!X2) {
             const size_t x2 = (size_t)g.nz * py * CHP * 3;
@@ -579,8 +584,8 @@ int DemagPlan::finish_spectra(bool symmetric, cudaStream_t st) {
         }
         CH = 1;
         CHP = 1;
-        blk = (long long)g.nz * g.ny * 3;
-        xblk = blk;
+        blk = (long long)CHr * nz_l * g.ny * 3;
+        xblk = (long long)nz_l * g.ny * 3;
         kmode = 4;
         longy = true;
         MXB_CUDA(cudaStreamSynchronize(st));
@@ -627,7 +632,7 @@ int DemagPlan::x_forward(const double* m, cudaStream_t st, const int* halt) {
     const int nx = g.nx;
     int rc = -1;
     static const bool rm_t = !(getenv("MXB_LONGY_RMT") && getenv("MXB_LONGY_RMT")[0] == '0');
-    if (longy && rm_t) {
+    if (longy && rm_t && G == 1) {
         // row-major r2c into X2 (free until the y forward), then a tiled transpose
         // into the plane-major XR (longy.cu)
         rc = fast_rows(true, px / 2, m, X2, nullptr, Nl, nx, nx / 2, hx, hxp, (long long)g.nz * g.ny * hxp * 3, rows,
@@ -678,15 +683,15 @@ int DemagPlan::yz(cudaStream_t st, const int* halt, cudaEvent_t* ev) {
     }
     if (longy) {
         // y forward (rows (kx, z): ny -> py), fused z over ky-contiguous tiles, y inverse
-        const long long rows = (long long)hx * nz;
-        if ((rc = longy_rows(-1, py, XR, X2, ny, py, rows, ply.tw, st, halt))) return rc;
+        const long long rows = (long long)kxn * nz;   // the rank's planes (all hx on one rank)
+        if ((rc = longy_rows(-1, py, XR, X2, ny, py, rows, ply.tw, st, halt, nz, nz_l, blk))) return rc;
         mark(2);
-        FusedArgs a{X2, Kp, nz, (long long)py * 3, py, 0, hx, (long long)nz * py * 3, scale, 1};
+        FusedArgs a{X2, Kp, nz, (long long)py * 3, py, 0, kxn, (long long)nz * py * 3, scale, 1};
         rc = fast_fused(pz, 4, a, plz.tw, st, halt);
         if (rc == -1) { set_error("no fused kernel for this shape"); rc = MXB_EINVAL; }
         if (rc) return rc;
         mark(3);
-        if ((rc = longy_rows(1, py, X2, XR, py, ny, rows, ply.tw, st, halt))) return rc;
+        if ((rc = longy_rows(1, py, X2, XR, py, ny, rows, ply.tw, st, halt, nz, nz_l, blk))) return rc;
         mark(4);
         return MXB_OK;
     }

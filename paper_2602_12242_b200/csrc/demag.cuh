@@ -45,8 +45,9 @@ int pipe_complex(const double2* K, double2* Kx, int L, int hx, int hxp, cudaStre
 // long y lines (longy.cu)
 bool longy_shape_ok(int py);
 int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
-               const double2* tw, cudaStream_t st, const int* halt);
-int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st);
+               const double2* tw, cudaStream_t st, const int* halt, int nz = 1, int nzl = 0,
+               long long gstride = 0);
+int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st, int kx0 = 0);
 int longy_rm_to_pm(const double2* in, double2* out, int ny, int nz, int hx, int hxp, cudaStream_t st);
 
 struct DemagPlan {

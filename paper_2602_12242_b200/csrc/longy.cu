@@ -1,4 +1,5 @@
-// Long y lines (py = 2048 / 4096, e.g. the 2048 x 2048 x 64 film), single rank.
+// Long y lines (py = 2048 / 4096, e.g. the 2048 x 2048 x 64 film), one rank or
+// a z slab (each rank its kx chunk, rows read from the all-to-all blocks).
 //
 // The 5-pass path keeps the spectra row-major, X[z][y][kx][c]: a y column is
 // 16 B every CHP*48 B (98 KB apart at hx = 2049) and two 4096-point lines per
@@ -34,17 +35,32 @@ template <int L> struct YRowCfg {
 constexpr unsigned kChunk = 32768;   // bytes per bulk copy
 }  // namespace
 
+// the XR side of a row (kx, z) = blockIdx.x = kx * nz + z: contiguous rows on
+// one rank; on a z slab the all-to-all receive blocks [g][kx][z_l][y][3]
+// (row z of plane kx in block z / nzl, nzl a power of two; zjump = block
+// stride / nzl), as the plane pipeline reads them
+struct YRowSlab {
+    int nz, nzl;
+    long long zjump;
+    __device__ long long row(long long r, int n) const {
+        const long long kx = r / nz;
+        const int z = (int)(r - kx * nz), zl = nzl == nz ? z : (z & (nzl - 1));
+        return (long long)(z - zl) * zjump + (kx * nzl + zl) * (long long)n * 3;
+    }
+};
+
 template <int L, int DIR>
 __global__ void __launch_bounds__(YRowCfg<L>::T, 1)
 k_yrow(const double2* __restrict__ in, double2* __restrict__ out, int n_in, int n_out,
-       const double2* __restrict__ tw, const int* __restrict__ halt) {
+       const double2* __restrict__ tw, const int* __restrict__ halt, YRowSlab sl) {
     if (halt && *halt) return;
     constexpr int R = YRowCfg<L>::R, TPL = YRowCfg<L>::TPL;
     extern __shared__ __align__(128) double2 X[];
     __shared__ alignas(8) unsigned long long mbar;
     const long long row = blockIdx.x;
-    const double2* src = in + row * (long long)n_in * 3;
-    double2* dst = out + row * (long long)n_out * 3;
+    // forward: XR (slab rows) -> X2 (local rows); inverse: X2 -> XR
+    const double2* src = in + (DIR < 0 ? sl.row(row, n_in) : row * (long long)n_in * 3);
+    double2* dst = out + (DIR < 0 ? row * (long long)n_out * 3 : sl.row(row, n_out));
     const int b = threadIdx.x / TPL, t = threadIdx.x - b * TPL;
     if (threadIdx.x == 0) {
         mbar_init(&mbar);
@@ -83,14 +99,14 @@ k_yrow(const double2* __restrict__ in, double2* __restrict__ out, int n_in, int 
 
 template <int L, int DIR>
 static int yrow_launch(const double2* in, double2* out, int n_in, int n_out, long long rows, const double2* tw,
-                       cudaStream_t st, const int* halt) {
+                       cudaStream_t st, const int* halt, YRowSlab sl) {
     const size_t smem = (size_t)YRowCfg<L>::XE * sizeof(double2);
     static bool attr = false;
     if (!attr) {
         MXB_CUDA(cudaFuncSetAttribute(k_yrow<L, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_yrow<L, DIR><<<(unsigned)rows, YRowCfg<L>::T, smem, st>>>(in, out, n_in, n_out, tw, halt);
+    k_yrow<L, DIR><<<(unsigned)rows, YRowCfg<L>::T, smem, st>>>(in, out, n_in, n_out, tw, halt, sl);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
@@ -98,11 +114,17 @@ static int yrow_launch(const double2* in, double2* out, int n_in, int n_out, lon
 bool longy_shape_ok(int py) { return py == 2048 || py == 4096; }
 
 int longy_rows(int dir, int L, const double2* in, double2* out, int n_in, int n_out, long long rows,
-               const double2* tw, cudaStream_t st, const int* halt) {
-    if (L == 2048) return dir < 0 ? yrow_launch<2048, -1>(in, out, n_in, n_out, rows, tw, st, halt)
-                                  : yrow_launch<2048, 1>(in, out, n_in, n_out, rows, tw, st, halt);
-    if (L == 4096) return dir < 0 ? yrow_launch<4096, -1>(in, out, n_in, n_out, rows, tw, st, halt)
-                                  : yrow_launch<4096, 1>(in, out, n_in, n_out, rows, tw, st, halt);
+               const double2* tw, cudaStream_t st, const int* halt, int nz, int nzl, long long gstride) {
+    if (nzl <= 0) nzl = nz;
+    if (nzl != nz && ((nzl & (nzl - 1)) || nz % nzl || gstride % nzl)) {
+        set_error("long-y slab: the local planes must be a power of two dividing nz");
+        return MXB_EINVAL;
+    }
+    const YRowSlab sl{nz, nzl, nzl != nz ? gstride / nzl : 0};
+    if (L == 2048) return dir < 0 ? yrow_launch<2048, -1>(in, out, n_in, n_out, rows, tw, st, halt, sl)
+                                  : yrow_launch<2048, 1>(in, out, n_in, n_out, rows, tw, st, halt, sl);
+    if (L == 4096) return dir < 0 ? yrow_launch<4096, -1>(in, out, n_in, n_out, rows, tw, st, halt, sl)
+                                  : yrow_launch<4096, 1>(in, out, n_in, n_out, rows, tw, st, halt, sl);
     set_error("no long-y row kernel for this length");
     return MXB_EINVAL;
 }
@@ -141,7 +163,7 @@ int longy_rm_to_pm(const double2* in, double2* out, int ny, int nz, int hx, int 
 // K (complex full spectra [kz][ky][hxp][6], exactly real) -> Kp[kx][ky'][kz'][6],
 // ky' <= py/2, kz' <= pz/2
 __global__ void k_quarter_kx_major(const double2* __restrict__ K, double* __restrict__ Kp, int py, int pz,
-                                   int hx, int hxp) {
+                                   int hx, int hxp, int kx0) {
     const int Y2 = py / 2 + 1, Z2 = pz / 2 + 1;
     const long long tot = (long long)hx * Y2 * Z2 * 6;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
@@ -152,12 +174,12 @@ __global__ void k_quarter_kx_major(const double2* __restrict__ K, double* __rest
         r /= Z2;
         const int ky = (int)(r % Y2);
         const int kx = (int)(r / Y2);
-        Kp[i] = K[(((long long)kz * py + ky) * hxp + kx) * 6 + c].x;
+        Kp[i] = K[(((long long)kz * py + ky) * hxp + kx0 + kx) * 6 + c].x;
     }
 }
 
-int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st) {
-    k_quarter_kx_major<<<148 * 8, 256, 0, st>>>(K, Kp, py, pz, hx, hxp);
+int longy_quarter(const double2* K, double* Kp, int py, int pz, int hx, int hxp, cudaStream_t st, int kx0) {
+    k_quarter_kx_major<<<148 * 8, 256, 0, st>>>(K, Kp, py, pz, hx, hxp, kx0);
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }

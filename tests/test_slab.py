@@ -22,7 +22,9 @@ NX, NY, NZ = 16, 8, 8
 # pipe512 / pipe1024 run the reference's tensor (complex-spectra pipeline, kernel
 # mode 5); pipe1024sym the mirrored GPU build (kernel mode 3, the bench's mode),
 # checked against the single-domain oracle on the spectra of the same build
-PIPE_DIMS = {"pipe512": (8, 256, 256), "pipe1024": (8, 512, 512), "pipe1024sym": (8, 512, 512)}
+PIPE_DIMS = {"pipe512": (8, 256, 256), "pipe1024": (8, 512, 512), "pipe1024sym": (8, 512, 512),
+             # long y lines (py = 2048, the film's path: k_yrow + the fused z pass), mirrored build
+             "longysym": (8, 1024, 8)}
 CELL = (2e-9, 2.5e-9, 3e-9)
 DT = 2e-14
 NSTEPS = 3
@@ -106,7 +108,7 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    if case in PIPE_DIMS:
+    if case in PIPE_DIMS and not case.startswith("longy"):
         os.environ["MXB_PIPE"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2602_12242_b200.slab import Comm, SlabPlan, SlabSimulation
@@ -139,7 +141,9 @@ def _worker(rank, world, port, kind, out, case="uniform", check_every=16):
             L.check(L.load().mxb_demag_set_packed(h, L.dptr(np.ascontiguousarray(packed))))
         km = C.c_int()
         L.check(L.load().mxb_demag_kmode(h, C.byref(km)))
-        if case in PIPE_DIMS:
+        if case.startswith("longy"):
+            assert km.value == 4, km.value       # long-y path on the rank's kx chunk
+        elif case in PIPE_DIMS:
             # plane pipeline: mirrored build -> real quarter (3), reference tensor -> complex (5)
             assert km.value == (3 if case.endswith("sym") else 5), km.value
         b = CudaSlabBackend(plan, gl, mat_l, h, 0)
@@ -185,7 +189,8 @@ def test_slab_numpy_gloo_matches_single_domain(case, check_every, world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case,world", [("uniform", 2), ("disk", 2), ("disk", 4), ("pipe512", 2), ("pipe512", 4),
-                                        ("pipe1024", 2), ("pipe1024sym", 2), ("pipe1024sym", 4)])
+                                        ("pipe1024", 2), ("pipe1024sym", 2), ("pipe1024sym", 4),
+                                        ("longysym", 2), ("longysym", 4)])
 def test_slab_cuda_ranks_match_single_domain(case, world):
     """disk: per-cell Ms and A across the slab faces (the neighbours' material
     planes are swapped once at start), cubic anisotropy and bulk DMI.
