@@ -77,6 +77,7 @@ struct mxb_ctx {
         cudaGraphExec_t exec;
     };
     std::vector<Graph> graphs;
+    std::vector<std::vector<double>> seen_keys;   // configurations whose first step ran eagerly
     Ctl* ctl = nullptr;
     double* partials = nullptr;
     int last_nparts = 0;          // partials of the last mxb_stage_dev final stage
@@ -1152,12 +1153,32 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
     static const bool graphs_on = getenv("MXB_GRAPHS") == nullptr || atoi(getenv("MXB_GRAPHS")) != 0;
     const bool use_graph = graphs_on && !ra->stage_bias && !ra->stage_bias_fields;
     for (int64_t k = 0; k < ra->nsteps; ++k) {
-        if (use_graph && k > 0) {
-            std::vector<double> key = {(double)t->mask, (double)t->ghost_mode, (double)t->precession,
-                                       (double)t->damping, (double)ra->method, (double)ra->renorm_each_stage,
-                                       (double)c->exact, (double)c->cur, ra->dt, ra->theta,
-                                       a.bias[0], a.bias[1], a.bias[2], (double)(uintptr_t)a.bias_field,
-                                       (double)(d ? d->uid : 0), (double)ra->fast_mask};
+        // the first step of a configuration runs eagerly (attribute setup, first
+        // launches); after that its step is captured once and replayed -- also
+        // across calls, so a run driven one step per call (sample_every = 1)
+        // replays graphs too
+        std::vector<double> key;
+        bool replay = false;
+        if (use_graph) {
+            key = {(double)t->mask, (double)t->ghost_mode, (double)t->precession,
+                   (double)t->damping, (double)ra->method, (double)ra->renorm_each_stage,
+                   (double)c->exact, (double)c->cur, ra->dt, ra->theta,
+                   a.bias[0], a.bias[1], a.bias[2], (double)(uintptr_t)a.bias_field,
+                   (double)(d ? d->uid : 0), (double)ra->fast_mask};
+            if (k > 0) {
+                replay = true;
+            } else {
+                for (const auto& gr : c->graphs) replay = replay || gr.key == key;
+                if (!replay) {
+                    for (const auto& sk : c->seen_keys) replay = replay || sk == key;
+                    if (!replay) {
+                        if (c->seen_keys.size() >= 2 * kMaxGraphs) c->seen_keys.erase(c->seen_keys.begin());
+                        c->seen_keys.push_back(key);
+                    }
+                }
+            }
+        }
+        if (replay) {
             cudaGraphExec_t ex = nullptr;
             for (size_t gi = 0; gi < c->graphs.size(); ++gi)
                 if (c->graphs[gi].key == key) {
