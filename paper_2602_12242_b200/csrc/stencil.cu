@@ -700,6 +700,9 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
 #ifndef MXB_ZC   // z planes per CTA; 512^3 stage time per step: 8 -> 14.37 ms, 16 -> 13.73, 32 -> 13.43, 64 -> 13.35
 #define MXB_ZC 32
 #endif
+#ifndef MXB_ZT_MINB   // CTAs per SM the TMA z-march is compiled for (register budget)
+#define MXB_ZT_MINB 2
+#endif
 #ifndef MXB_ZM_CTAS
 #define MXB_ZM_CTAS 3
 #endif
@@ -850,7 +853,7 @@ template <int MODE> struct ZtAux {
 };
 
 template <int MODE, bool E>
-__global__ void __launch_bounds__(ZTX * ZTY, 2) k_stage_zt(StageArgs a, const __grid_constant__ ZtMaps maps,
+__global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a, const __grid_constant__ ZtMaps maps,
                                                             int nfields, int has_hd) {
     if (a.halt && *(volatile const int*)a.halt) return;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
