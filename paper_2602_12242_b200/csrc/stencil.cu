@@ -694,14 +694,14 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
 // tile with a one-cell halo ring, z neighbours stay in registers.  Same
 // neighbour values, face coefficients and arithmetic as k_stage.
 // ---------------------------------------------------------------------------
-#ifndef MXB_ZTY
-#define MXB_ZTY 8
+#ifndef MXB_ZTY   // tile rows: 32 x 4 tiles at 4 CTAs per SM beat 32 x 8 at 2 (12.3 vs 12.9 ms per step)
+#define MXB_ZTY 4
 #endif
-#ifndef MXB_ZC   // z planes per CTA; 512^3 stage time per step: 8 -> 14.37 ms, 16 -> 13.73, 32 -> 13.43, 64 -> 13.35
-#define MXB_ZC 32
+#ifndef MXB_ZC   // z planes per CTA; 512^3 stage time per step (32 x 8 tiles): 8 -> 14.37 ms, 16 -> 13.73,
+#define MXB_ZC 64  // 32 -> 13.43, 64 -> 13.35; 32 x 4 tiles: 32 -> 12.45, 64 -> 12.33
 #endif
 #ifndef MXB_ZT_MINB   // CTAs per SM the TMA z-march is compiled for (register budget)
-#define MXB_ZT_MINB 2
+#define MXB_ZT_MINB (16 / MXB_ZTY)
 #endif
 #ifndef MXB_ZM_CTAS
 #define MXB_ZM_CTAS 3
