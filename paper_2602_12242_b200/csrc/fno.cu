@@ -80,6 +80,112 @@ __global__ void k_fno_dft_x(const double* __restrict__ v, double2* __restrict__ 
     A[t] = make_double2(re, im);
 }
 
+// Blocked forms of the two large passes (the per-output loops above re-read the
+// twiddle table and the input row m2 / w times from L2; at 2048^2 they were
+// ~95% of the forward pass):
+//   k_fno_dft_x_w: one warp per row, lanes over x, all m2 <= 12 outputs
+//   accumulated in registers against table chunks staged in shared memory,
+//   warp-shuffle reduction at the end;
+//   k_fno_block_out_t: one thread per x of a row, the w <= MAXW input channels
+//   of that cell in registers, C[:, y, :], the bypass weights and a table chunk
+//   in shared memory, all w outputs from one pass.
+constexpr int kFnoChunk = 128;   // x values per staged table chunk
+
+template <int MAXM2>
+__global__ void __launch_bounds__(256) k_fno_dft_x_w(const double* __restrict__ v, double2* __restrict__ A,
+                                                     const double2* __restrict__ ex, int rows, int W, int m2) {
+    __shared__ double2 es[MAXM2][kFnoChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long row = (long long)blockIdx.x * 8 + warp;
+    const double* vr = v + row * W;
+    double2 acc[MAXM2];
+#pragma unroll
+    for (int k = 0; k < MAXM2; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (int x0 = 0; x0 < W; x0 += kFnoChunk) {
+        const int n = min(kFnoChunk, W - x0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m2 * kFnoChunk; i += 256) {
+            const int k = i / kFnoChunk, x = i - k * kFnoChunk;
+            if (x < n) es[k][x] = __ldg(ex + (long long)k * W + x0 + x);
+        }
+        __syncthreads();
+        if (row < rows) {
+            for (int x = lane; x < n; x += 32) {
+                const double a = __ldg(vr + x0 + x);
+#pragma unroll
+                for (int k = 0; k < MAXM2; ++k)
+                    if (k < m2) {
+                        acc[k].x = fma(a, es[k][x].x, acc[k].x);
+                        acc[k].y = fma(a, es[k][x].y, acc[k].y);
+                    }
+            }
+        }
+    }
+    if (row >= rows) return;
+#pragma unroll
+    for (int k = 0; k < MAXM2; ++k) {
+        if (k >= m2) break;
+        double re = acc[k].x, im = acc[k].y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0) A[row * m2 + k] = make_double2(re, im);
+    }
+}
+
+template <int MAXW, int MAXM2>
+__global__ void __launch_bounds__(kFnoChunk) k_fno_block_out_t(const double2* __restrict__ C, const double* __restrict__ vin,
+                                                               double* __restrict__ vout, const double2* __restrict__ ex,
+                                                               const double* __restrict__ lw, const double* __restrict__ lb,
+                                                               int w, int H, int W, int m2, int act, double scale) {
+    __shared__ double2 cs[MAXW][MAXM2];
+    __shared__ double2 es[MAXM2][kFnoChunk];
+    __shared__ double ws[MAXW][MAXW + 1];
+    __shared__ double bs[MAXW];
+    const long long HW = (long long)H * W;
+    const int y = blockIdx.y, x0 = blockIdx.x * kFnoChunk, x = x0 + threadIdx.x;
+    for (int i = threadIdx.x; i < w * m2; i += kFnoChunk) {
+        const int o = i / m2, k = i - o * m2;
+        cs[o][k] = C[((long long)o * H + y) * m2 + k];
+    }
+    for (int i = threadIdx.x; i < m2 * kFnoChunk; i += kFnoChunk) {
+        const int k = i / kFnoChunk, xx = i - k * kFnoChunk;
+        if (x0 + xx < W) es[k][xx] = __ldg(ex + (long long)k * W + x0 + xx);
+    }
+    if (lw) {
+        for (int i = threadIdx.x; i < w * w; i += kFnoChunk) ws[i / w][i % w] = lw[i];
+        for (int i = threadIdx.x; i < w; i += kFnoChunk) bs[i] = lb[i];
+    }
+    __syncthreads();
+    if (x >= W) return;
+    const long long p = (long long)y * W + x;
+    double vi[MAXW];
+#pragma unroll
+    for (int i = 0; i < MAXW; ++i) vi[i] = (lw && i < w) ? __ldg(vin + i * HW + p) : 0.0;
+    for (int o = 0; o < w; ++o) {
+        double s = cs[o][0].x;
+#pragma unroll
+        for (int k = 1; k < MAXM2; ++k)
+            if (k < m2) {
+                const double2 z = cs[o][k], e = es[k][threadIdx.x];
+                s += 2.0 * (z.x * e.x + z.y * e.y);
+            }
+        s *= scale;
+        double r = s;
+        if (lw) {
+            double l = 0.0;
+#pragma unroll
+            for (int i = 0; i < MAXW; ++i)
+                if (i < w) l = fma(ws[o][i], vi[i], l);
+            r = s + (l + bs[o]);
+        }
+        if (act >= 0) r = act_fn(r, act);
+        vout[o * HW + p] = r;
+    }
+}
+
 // X[c][r][kx] = sum_y A[c][y][kx] ey[r][y]
 __global__ void k_fno_dft_y(const double2* __restrict__ A, double2* __restrict__ X, const double2* __restrict__ ey,
                             int w, int H, int m1, int m2) {
@@ -231,12 +337,21 @@ static int fno_block(FnoDev& f, const double* vin, double* vout, const double2* 
                      const double* lw, const double* lb, int act) {
     const int T = 256, w = f.w, R = 2 * f.m1;
     const long long HW = (long long)f.H * f.W;
-    k_fno_dft_x<<<nblk((long long)w * f.H * f.m2, T), T, 0, f.st>>>(vin, f.A, f.ex, w * f.H, f.W, f.m2);
+    if (f.m2 <= 12)
+        k_fno_dft_x_w<12><<<nblk((long long)w * f.H, 8), 256, 0, f.st>>>(vin, f.A, f.ex, w * f.H, f.W, f.m2);
+    else
+        k_fno_dft_x<<<nblk((long long)w * f.H * f.m2, T), T, 0, f.st>>>(vin, f.A, f.ex, w * f.H, f.W, f.m2);
     k_fno_dft_y<<<nblk((long long)w * R * f.m2, T), T, 0, f.st>>>(f.A, f.Xf, f.ey, w, f.H, f.m1, f.m2);
     k_fno_mix<<<nblk((long long)w * R * f.m2, T), T, 0, f.st>>>(f.Xf, f.Yf, wp, wn, w, f.m1, f.m2);
     k_fno_idft_y<<<nblk((long long)w * f.H * f.m2, T), T, 0, f.st>>>(f.Yf, f.C, f.ey, w, f.H, f.m1, f.m2);
-    k_fno_block_out<<<nblk((long long)w * HW, T), T, 0, f.st>>>(f.C, vin, vout, f.ex, lw, lb, w, f.H, f.W, f.m2,
-                                                                act, 1.0 / ((double)f.H * f.W));
+    if (w <= 32 && f.m2 <= 12) {
+        const dim3 grid((unsigned)((f.W + kFnoChunk - 1) / kFnoChunk), (unsigned)f.H);
+        k_fno_block_out_t<32, 12><<<grid, kFnoChunk, 0, f.st>>>(f.C, vin, vout, f.ex, lw, lb, w, f.H, f.W, f.m2,
+                                                               act, 1.0 / ((double)f.H * f.W));
+    } else {
+        k_fno_block_out<<<nblk((long long)w * HW, T), T, 0, f.st>>>(f.C, vin, vout, f.ex, lw, lb, w, f.H, f.W,
+                                                                    f.m2, act, 1.0 / ((double)f.H * f.W));
+    }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
 }
