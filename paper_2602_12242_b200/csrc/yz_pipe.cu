@@ -85,6 +85,9 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
+#ifndef MXB_PIPE_KPRE       // B: first kernel entry loaded before the spectrum store + barrier
+#define MXB_PIPE_KPRE 0
+#endif
 #ifndef MXB_PIPE_SEEN       // skip re-acquiring a plane counter this CTA already saw complete
 #define MXB_PIPE_SEEN 0
 #endif
@@ -790,6 +793,14 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             } else {
                 // ---- B: * K between the z forward and z inverse of column ky = idx
                 const int ky = cur.idx;
+#if MXB_PIPE_KPRE && MXB_PIPE_KPAIR
+                // this thread's first kernel entry (q = threadIdx.x <= L/2), loaded before
+                // the spectrum goes to shared memory: its latency overlaps the stores and
+                // the barrier
+                const double2* kpre = Kp2 + ((long long)cur.plane * L2 + (2 * ky > L ? L - ky : ky)) * L2 * 3 +
+                                      threadIdx.x * 3;
+                const double2 pre01 = __ldg(kpre), pre23 = __ldg(kpre + 1), pre45 = __ldg(kpre + 2);
+#endif
                 __syncwarp();
 #pragma unroll
                 for (int k = 0; k < 32; ++k) Wc[lane + 32 * k] = v[fw::p32(k)];
@@ -814,7 +825,18 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #endif
                 for (int q = a.cplx ? L : threadIdx.x; q <= L / 2; q += 96) {
                     const double2* kr = krow + q * 3;
+#if MXB_PIPE_KPRE
+                    double2 q01, q23, q45;
+                    if (q == (int)threadIdx.x) {
+                        q01 = pre01; q23 = pre23; q45 = pre45;
+                    } else {
 #if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                        q01 = ldg_hint(kr, pk); q23 = ldg_hint(kr + 1, pk); q45 = ldg_hint(kr + 2, pk);
+#else
+                        q01 = __ldg(kr); q23 = __ldg(kr + 1); q45 = __ldg(kr + 2);
+#endif
+                    }
+#elif MXB_PIPE_HINTS && MXB_PIPE_HINT_K
                     const double2 q01 = ldg_hint(kr, pk), q23 = ldg_hint(kr + 1, pk), q45 = ldg_hint(kr + 2, pk);
 #else
                     const double2 q01 = __ldg(kr), q23 = __ldg(kr + 1), q45 = __ldg(kr + 2);
