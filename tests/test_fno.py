@@ -303,3 +303,20 @@ def test_surrogate_runs_inside_the_device_loop(tmp_path):
     for k in ("mx", "my", "mz"):
         assert np.max(np.abs(tr.column(k) - tr_h.column(k))) <= 1e-12
     assert tr.counters["demag"] == tr_h.counters["demag"] == 80
+
+
+@gpu
+@pytest.mark.parametrize("width,modes,H,W", [(4, (3, 3), 24, 200), (32, (12, 12), 40, 260), (8, (5, 7), 33, 129)])
+def test_blocked_passes_odd_shapes_match_oracle(width, modes, H, W):
+    """The blocked x-DFT (table chunks of 128 x values) and the fused block
+    output (128-column tiles) on widths that are not multiples of the chunk,
+    row counts that are not multiples of the 8 rows per CTA, odd H: against the
+    oracle restatement (oracle/fno_oracle.py, pinned to the reference)."""
+    from oracle import fno_oracle as FO
+    from tests.fno_tables import tensors
+    t = tensors(width, modes, 31)
+    model = F.FnoModel.from_tensors(t).freeze()
+    x = np.random.default_rng(32).standard_normal((3, H, W))
+    y = model.infer(x)
+    ref = FO.infer(t, x, model.activation)
+    assert rel(y, ref) <= 1e-12
