@@ -85,6 +85,12 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
+#ifndef MXB_PIPE_LATE_SIGNAL   // signal the previous unit mid-unit (after the next ticket), not before compute
+#define MXB_PIPE_LATE_SIGNAL 0
+#endif
+#ifndef MXB_PIPE_NOBAR      // with the late signal: no CTA barrier after the staging wait
+#define MXB_PIPE_NOBAR 0
+#endif
 #ifndef MXB_PIPE_KPRE       // B: first kernel entry loaded before the spectrum store + barrier
 #define MXB_PIPE_KPRE 0
 #endif
@@ -737,6 +743,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #endif
         stage(cur);
         stage_wait(cur);
+#if !MXB_PIPE_LATE_SIGNAL
         if (pending.kind != U_NONE) {
             if (threadIdx.x == 0) {
                 // a B unit's column went out as TMA stores: complete them first
@@ -746,7 +753,12 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             sc.signal(pending);
             pending.kind = U_NONE;
         }
+#endif
+#if !(MXB_PIPE_LATE_SIGNAL && MXB_PIPE_NOBAR)
+        // (with the late signal nothing here needs the CTA: every thread has waited
+        // for the staged input on the mbarrier itself)
         __syncthreads();
+#endif
         double2* slot = a.slot + (long long)(cur.plane % 3) * slot_e;
 #if MXB_PIPE_DISCARD && !MXB_PIPE_DISCARD_LATE
         if (cur.kind == U_C) {
@@ -779,6 +791,16 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #endif
 #if MXB_PIPE_EARLY_READY
                 early = early_read(next_ticket);
+#endif
+#if MXB_PIPE_LATE_SIGNAL
+                // the previous unit's completion, off the critical path: its bulk /
+                // TMA stores finished long ago; no blocking wait lies between
+                if (pending.kind != U_NONE) {
+                    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    sc.signal(pending);
+                    pending.kind = U_NONE;
+                }
 #endif
             }
             if (cur.kind == U_A) {
@@ -909,6 +931,16 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #endif
 #if MXB_PIPE_EARLY_READY
                     early = early_read(next_ticket);
+#endif
+#if MXB_PIPE_LATE_SIGNAL
+                    // the previous unit's completion, off the critical path: its bulk /
+                    // TMA stores finished long ago; no blocking wait lies between
+                    if (pending.kind != U_NONE) {
+                        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        sc.signal(pending);
+                        pending.kind = U_NONE;
+                    }
 #endif
                 }
 #if MXB_PIPE_W_DIRECT_STORE
