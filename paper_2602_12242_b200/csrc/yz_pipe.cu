@@ -88,6 +88,9 @@
 #ifndef MXB_PIPE_LATE_SIGNAL   // signal the previous unit mid-unit (after the next ticket), not before compute
 #define MXB_PIPE_LATE_SIGNAL 0
 #endif
+#ifndef MXB_PIPE_SIGNAL_EARLY   // signal the previous unit between this unit's TMA issue and its wait
+#define MXB_PIPE_SIGNAL_EARLY 0
+#endif
 #ifndef MXB_PIPE_NOBAR      // with the late signal: no CTA barrier after the staging wait
 #define MXB_PIPE_NOBAR 0
 #endif
@@ -742,6 +745,19 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         if (!sc.wait_ready(cur, &flag, pending)) return;
 #endif
         stage(cur);
+#if MXB_PIPE_SIGNAL_EARLY
+        // the previous unit's completion while this unit's input is in flight: the
+        // wait for its stores to complete overlaps the TMA latency, and consumers
+        // see the signal one staging wait earlier
+        if (pending.kind != U_NONE) {
+            if (threadIdx.x == 0) {
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            sc.signal(pending);
+            pending.kind = U_NONE;
+        }
+#endif
         stage_wait(cur);
 #if !MXB_PIPE_LATE_SIGNAL
         if (pending.kind != U_NONE) {
