@@ -925,6 +925,29 @@ int mxb_state_energies(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_b
 
 // enqueue one step reading Yb[cur] and writing Yb[cur^1]; stage bias rows
 // `sb` (4 or 1 rows of 3) or the constant a0.bias
+// the kernel-selection switches read per launch (tests flip them between runs):
+// part of a captured step's key, so a cached graph never replays another path
+static double env_sig() {
+    uint64_t h = 1469598103934665603ull;
+    for (const char* n : {"MXB_XFUSE", "MXB_ZTMA", "MXB_XWARP"}) {
+        const char* v = getenv(n);
+        for (const char* q = v ? v : "\x01"; *q; ++q) h = (h ^ (unsigned char)*q) * 1099511628211ull;
+        h = (h ^ 0xffu) * 1099511628211ull;
+    }
+    return (double)(h >> 12);
+}
+
+// the x-row fused stages apply: single-rank plane pipeline with the warp x
+// kernels at nx = 512, and a stage the fused kernel covers (stencil.cu)
+static bool xstage_on(const mxb_ctx* c, const mxb_demag* d, const StageArgs& a) {
+    (void)c;
+    const DemagPlan& p = d->plan;
+    const char* xw = getenv("MXB_XWARP");
+    if (d->fno || (xw && xw[0] == '0')) return false;
+    return p.G == 1 && p.pipe && p.fast && p.px == 1024 && p.CH == 1 && p.XS == p.XR && p.has_kernel &&
+           xstage_eligible(a);
+}
+
 static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int method, double dt,
                         const double* sb, bool renorm_stage, bool use_demag, const double* sbf = nullptr) {
     const double* y = c->Yb[c->cur];
@@ -963,6 +986,28 @@ static int enqueue_step(mxb_ctx* c, mxb_demag* d, const StageArgs& a0, int metho
         return launch_stage(M_EULER, c->exact, a, c->st);
     }
     const double half = 0.5 * dt;
+    if (use_demag && xstage_on(c, d, a)) {
+        // x-row fused stages (stencil.cu k_stage_x): H_demag never leaves the SM and
+        // stages 1-3 write the next evaluation's x spectra themselves
+        const XStage xs{d->plan.XS, d->plan.xblk, d->plan.plm.tw, d->plan.plx.tw};
+        DemagPlan& pl = d->plan;
+        if ((rc = pl.x_forward(y, c->st, halt))) return rc;
+        const double* ys_[4] = {y, c->P, ynew, c->P};
+        double* out_[4] = {c->P, ynew, c->P, ynew};
+        const double cf[4] = {half, half, dt, dt};
+        const int mode_[4] = {M_RK1, M_RK2, M_RK3, M_RK4};
+        for (int s4 = 0; s4 < 4; ++s4) {
+            if ((rc = pl.yz(c->st, halt))) return rc;
+            set_bias(s4);
+            if (brc) return brc;
+            a.ys = ys_[s4];
+            a.out = out_[s4];
+            a.c = cf[s4];
+            a.dt6 = dt / 6.0;
+            if ((rc = launch_xstage(mode_[s4], c->exact, a, xs, c->st))) return rc;
+        }
+        return MXB_OK;
+    }
     // stage 1: y -> P (y2)
     if (use_demag && (rc = demag_into(c, d, y, c->Hd, halt))) return rc;
     set_bias(0); a.ys = y; a.out = c->P; a.c = half;
@@ -1164,7 +1209,7 @@ int mxb_run(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_run_args* ra
                    (double)t->damping, (double)ra->method, (double)ra->renorm_each_stage,
                    (double)c->exact, (double)c->cur, ra->dt, ra->theta,
                    a.bias[0], a.bias[1], a.bias[2], (double)(uintptr_t)a.bias_field,
-                   (double)(d ? d->uid : 0), (double)ra->fast_mask};
+                   (double)(d ? d->uid : 0), (double)ra->fast_mask, env_sig()};
             if (k > 0) {
                 replay = true;
             } else {
@@ -1410,21 +1455,29 @@ int mxb_time_steps(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, double dt, int 
     MXB_CUDA(cudaMemcpy(&h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     if (h.halt) { set_error("timed steps halted (blow-up or dead cell)"); return h.halt; }
     // stencil-only timing: the same fused stage kernels without the FFTs
+    // (with the x-row fused stages: those kernels -- x c2r + stage + x r2c -- on the
+    // spectra the last step left, without the y/z pipeline; the state is scratch)
     if (ms_stencil) {
         a.halt = nullptr;
+        const bool xf = use_demag && xstage_on(c, d, a);
+        const XStage xs = xf ? XStage{d->plan.XS, d->plan.xblk, d->plan.plm.tw, d->plan.plx.tw} : XStage{};
+        auto stage = [&](int mode, const StageArgs& b) {
+            if (xf) launch_xstage(mode, c->exact, b, xs, c->st);
+            else launch_stage(mode, c->exact, b, c->st);
+        };
         cudaEventRecord(e0, c->st);
         for (int k = 0; k < nsteps; ++k) {
             StageArgs b = a;
             b.y = c->Yb[c->cur]; b.k1 = c->K1; b.k1_out = c->K1; b.s = c->S; b.hd = c->Hd;
             b.ctl = c->ctl; b.partials = c->partials;
             b.ys = b.y; b.out = c->P; b.c = 0.5 * dt;
-            launch_stage(M_RK1, c->exact, b, c->st);
+            stage(M_RK1, b);
             b.ys = c->P; b.out = c->Yb[c->cur ^ 1];
-            launch_stage(M_RK2, c->exact, b, c->st);
+            stage(M_RK2, b);
             b.ys = c->Yb[c->cur ^ 1]; b.out = c->P; b.c = dt;
-            launch_stage(M_RK3, c->exact, b, c->st);
+            stage(M_RK3, b);
             b.ys = c->P; b.out = c->Yb[c->cur ^ 1]; b.dt6 = dt / 6.0;
-            launch_stage(M_RK4, c->exact, b, c->st);
+            stage(M_RK4, b);
             c->cur ^= 1;
         }
         cudaEventRecord(e1, c->st);
@@ -1432,7 +1485,12 @@ int mxb_time_steps(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, double dt, int 
         cudaEventElapsedTime(&ms, e0, e1);
         *ms_stencil = ms;
     }
-    if (launches) *launches = (int64_t)nsteps * (4 * (1 + (use_demag ? d->plan.kernels_per_eval() : 0)) + 1);
+    if (launches) {
+        // x-row fused stages: one x forward, then per stage the y/z pipeline and the fused kernel
+        const bool xf = use_demag && xstage_on(c, d, a);
+        *launches = xf ? (int64_t)nsteps * (1 + 4 * 2 + 1)
+                       : (int64_t)nsteps * (4 * (1 + (use_demag ? d->plan.kernels_per_eval() : 0)) + 1);
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return MXB_OK;

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 
+#include "fft_warp.cuh"
 #include "stencil.cuh"
 #include "tma.cuh"
 
@@ -503,7 +504,7 @@ template <int MODE, bool E>
 __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, const CellMat& cm,
                                            const double m[3], const double h[3], double red[4],
                                            const double* y_pre = nullptr, const double* k1_pre = nullptr,
-                                           const double* s_pre = nullptr) {
+                                           const double* s_pre = nullptr, double* v_ret = nullptr) {
     const long long N = a.g.N;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
         if (MODE == M_HEFF) {
@@ -555,6 +556,7 @@ __device__ __forceinline__ void stage_tail(const StageArgs& a, long long idx, co
                 if (!renorm_cell<E>(v, cm)) flag_dead(a.ctl, idx);
             }
             a.out[idx] = v[0]; a.out[N + idx] = v[1]; a.out[2 * N + idx] = v[2];
+            if (v_ret) { v_ret[0] = v[0]; v_ret[1] = v[1]; v_ret[2] = v[2]; }
         }
     }
 }
@@ -1342,6 +1344,261 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
     StageArgs b = a;
     b.halt = nullptr;
     return launch_finalize(b, 2, st);
+}
+
+}  // namespace mxb
+
+// ---------------------------------------------------------------------------
+// x-row fused stage: the x c2r of the demag spectra, the stage update and (for
+// stages 1-3) the x r2c of the new stage state in ONE kernel, for the single-
+// rank plane pipeline at nx = 512 (north_star item 3: each stage streams M
+// once).  Without it a stage is k_c2r_w (writes H_demag, 24 B/cell), the
+// stage kernel (reads it back) and k_r2c_w (reads the new state again):
+// 72 B/cell per stage that never leave the SM here.
+//
+// A CTA is 3 warps and owns a row pair (rows 2b, 2b+1 of the nz*ny x-rows),
+// exactly the rows its plane-major spectrum slice X[kx][2b..2b+1][3] holds:
+//   1. TMA: the slice (513 x 96 B) into shared memory;
+//   2. c2r as k_c2r_w (x_warp.cu), one component per warp; H_demag of the
+//      pair stays in the first half of each warp's transpose tile;
+//   3. the stage update of the pair's 1024 cells (heff_nb + stage_tail: the
+//      arithmetic of k_stage_zt, bit-identical), neighbours read through L1/L2
+//      (the y +- 1 rows are the adjacent CTAs', the z +- 1 rows were read
+//      ny/2 CTAs earlier and are L2 hits); the new state also goes to the
+//      second half of the tiles;
+//   4. r2c of the new state as k_r2c_w, and the spectrum slice written back by
+//      TMA to the addresses step 1 read (each CTA owns its slice: in place).
+// Results are bit-identical to the unfused kernels; the final stage's block
+// partials are reduced per row pair.
+// ---------------------------------------------------------------------------
+namespace mxb {
+namespace {
+constexpr int XSM = 512;        // complex FFT length of the x rows (px / 2)
+constexpr int XSH = XSM + 1;    // spectrum bins (px / 2 + 1)
+}
+
+template <int MODE, bool E, bool R2C>
+__global__ void __launch_bounds__(96, 4)
+k_stage_x(StageArgs a, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
+          const __grid_constant__ CUtensorMap map_main, const __grid_constant__ CUtensorMap map_tail) {
+    if (a.halt && *(volatile const int*)a.halt) return;
+    constexpr bool kFinal = MODE == M_RK4;
+    constexpr bool kK1 = MODE == M_RK4, kS = MODE == M_RK3 || MODE == M_RK4;
+    extern __shared__ __align__(128) double2 S[];
+    __shared__ alignas(8) unsigned long long mbar;
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long row0 = 2LL * blockIdx.x;
+    const int xo0 = (int)(row0 * 6);
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar);
+        mbar_expect(&mbar, XSH * 96);
+        tma_load_2d(S, &map_main, xo0, 0, &mbar);
+        tma_load_2d(S + 256 * 6, &map_main, xo0, 256, &mbar);
+        tma_load_2d(S + 512 * 6, &map_tail, xo0, 512, &mbar);
+    }
+    __syncthreads();   // mbarrier initialised before anyone polls it
+    double2 fa[16], fb[16], v[32];
+    {
+        double2 twp[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) twp[m] = __ldg(tw1024 + lane + 32 * m);
+        mbar_wait(&mbar, 0);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int k = lane + 32 * m;
+            const double2 w = twp[m];
+#pragma unroll
+            for (int ln = 0; ln < 2; ++ln) {
+                const double2 xk = S[(k * 2 + ln) * 3 + c];
+                const double2 xm = S[((XSM - k) * 2 + ln) * 3 + c];
+                const double2 A = make_double2(xk.x + xm.x, xk.y - xm.y);
+                const double2 Bm = make_double2(xk.x - xm.x, xk.y + xm.y);
+                const double2 B = cmul(Bm, make_double2(w.x, -w.y));
+                const double2 z = make_double2(A.x - B.y, A.y + B.x);
+                if (ln == 0) fa[m] = z; else fb[m] = z;
+            }
+        }
+    }
+    __syncthreads();   // S becomes the transpose tiles
+    double2* tile = S + c * 1024;
+    fw::fft512x2<1>(fa, fb, v, tile, lane, tw512);
+    {
+        // H_demag of component c: (x[2n], x[2n+1]) pairs of both lines, first half of the tile
+        const int line = lane >> 4, k1 = lane & 15;
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) tile[line * 256 + k1 + 16 * k2] = v[fw::p32(k2)];
+    }
+    __syncthreads();
+    // the stage update of the pair's cells
+    const Grid& g = a.g;
+    const long long N = g.N, plane = (long long)g.nx * g.ny;
+    const CellMat cm = cell_mat<E, true>(a, 0);
+    const double hf = a.dv.face, Af = cm.A, p = cm.slope_p;
+    const double* hd_s = reinterpret_cast<const double*>(S);   // [q][2048]: H_demag at [ln * 512 + x]
+    double* out_s = reinterpret_cast<double*>(S) + 1024;       // [q][2048]: new state at [ln * 512 + x]
+    double red[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int e = threadIdx.x; e < 2 * XSM; e += 96) {
+        const int ln = e >> 9, i = e & (XSM - 1);
+        const long long row = row0 + ln;
+        const int k = (int)(row / g.ny), j = (int)(row - (long long)k * g.ny);
+        const long long idx = row * XSM + i;
+        const bool okxp = i + 1 < XSM, okxm = i > 0, okyp = j + 1 < g.ny, okym = j > 0;
+        const bool zp_ok = k + 1 < g.nz, zm_ok = k > 0;
+        double m[3], xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const long long o = q * N + idx;
+            m[q] = ld(a.ys, o);
+            xp[q] = okxp ? ld(a.ys, o + 1) : 0.0;
+            xm[q] = okxm ? ld(a.ys, o - 1) : 0.0;
+            yp[q] = okyp ? ld(a.ys, o + XSM) : 0.0;
+            ym[q] = okym ? ld(a.ys, o - XSM) : 0.0;
+            zp[q] = zp_ok ? ld(a.ys, o + plane) : 0.0;
+            zm[q] = zm_ok ? ld(a.ys, o - plane) : 0.0;
+        }
+        double yv[3], k1v[3], sv[3], hdv[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            yv[q] = ld(a.y, q * N + idx);
+            k1v[q] = kK1 ? ld(a.k1, q * N + idx) : 0.0;
+            sv[q] = kS ? a.s[q * N + idx] : 0.0;
+            hdv[q] = hd_s[q * 2048 + e];
+        }
+        if (!okxp) ghost_nb<E>(a, 0, +1, m, p, xp);
+        if (!okxm) ghost_nb<E>(a, 0, -1, m, p, xm);
+        if (!okyp) ghost_nb<E>(a, 1, +1, m, p, yp);
+        if (!okym) ghost_nb<E>(a, 1, -1, m, p, ym);
+        if (!zp_ok) ghost_nb<E>(a, 2, +1, m, p, zp);
+        if (!zm_ok) ghost_nb<E>(a, 2, -1, m, p, zm);
+        double h[3], vn[3];
+        heff_nb<E, true>(a, a.ys, idx, i, j, k, m, cm, a.terms, xp, xm, yp, ym, zp, zm,
+                         okxp ? hf : Af, okxm ? hf : Af, okyp ? hf : Af, okym ? hf : Af,
+                         zp_ok ? hf : Af, zm_ok ? hf : Af, h, hdv);
+        stage_tail<MODE, E>(a, idx, cm, m, h, red, yv, kK1 ? k1v : nullptr, kS ? sv : nullptr, vn);
+        if (R2C) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) out_s[q * 2048 + e] = vn[q];
+        }
+    }
+    if (kFinal) {
+        const bool is_max[4] = {false, false, false, true};
+        block_reduce<4>(red, is_max);
+        if (threadIdx.x == 0) {
+            double* pp = a.partials + (long long)blockIdx.x * kReduceSlots;
+            pp[0] = red[0]; pp[1] = red[1]; pp[2] = red[2]; pp[3] = red[3];
+        }
+    }
+    if (!R2C) return;
+    __syncthreads();   // the new state of the pair is staged
+    {
+        // packed pairs (x[2n], x[2n+1]) of component c, n < 256 non-zero (k_r2c_w)
+        const double2* s0 = tile + 512;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            fa[m] = m < 8 ? s0[lane + 32 * m] : make_double2(0.0, 0.0);
+            fb[m] = m < 8 ? s0[256 + lane + 32 * m] : make_double2(0.0, 0.0);
+        }
+    }
+    __syncwarp();      // the transposes below overwrite the warp's own tile only
+    fw::fft512x2<-1>(fa, fb, v, tile, lane, tw512);
+    {
+        const int line = lane >> 4, k1 = lane & 15;
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 32; ++k2) tile[line * XSM + k1 + 16 * k2] = v[fw::p32(k2)];
+        __syncwarp();
+    }
+    constexpr int NI = (XSH + 31) / 32;   // 17
+    double2 xo[2][NI];
+    const double2 w32 = tw1024[32];
+    double2 wk = tw1024[lane];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        if (i % 4 == 0) { if (i) wk = tw1024[lane + 32 * i]; }
+        else wk = cmul(wk, w32);
+#pragma unroll
+        for (int ln = 0; ln < 2; ++ln) {
+            const int kx = lane + 32 * i;
+            if (kx < XSH) {
+                const double2 zk = tile[ln * XSM + (kx & (XSM - 1))];
+                const double2 zm = tile[ln * XSM + ((XSM - kx) & (XSM - 1))];
+                const double2 Ev = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+                const double2 Od = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+                xo[ln][i] = cadd(Ev, cmul(wk, Od));
+            }
+        }
+    }
+    __syncthreads();   // every warp is done with its tile: stage the slice
+#pragma unroll
+    for (int ln = 0; ln < 2; ++ln)
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int kx = lane + 32 * i;
+            if (kx < XSH) S[(kx * 2 + ln) * 3 + c] = xo[ln][i];
+        }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tma_store_2d(&map_main, xo0, 0, S);
+        tma_store_2d(&map_main, xo0, 256, S + 256 * 6);
+        tma_store_2d(&map_tail, xo0, 512, S + 512 * 6);
+        bulk_commit();
+        bulk_wait_read();
+    }
+}
+
+bool xstage_eligible(const StageArgs& a) {
+    const char* e = getenv("MXB_XFUSE");   // read per call: tests switch it
+    if (e && e[0] == '0') return false;
+    const Grid& g = a.g;
+    return a.mat.uniform && a.mat.all_magnetic && a.ghost != MXB_GHOST_PERIODIC &&
+           !(a.terms & (MXB_TERM_CUBIC | MXB_TERM_BULK_DMI)) && (a.terms & MXB_TERM_DEMAG) &&
+           !a.halo_lo && !a.halo_hi && g.nx == XSM && ((long long)g.ny * g.nz) % 2 == 0;
+}
+
+template <int MODE, bool E, bool R2C>
+static void launch_x1(const StageArgs& a, const XStage& x, const CUtensorMap& mm, const CUtensorMap& mt,
+                      unsigned grid, cudaStream_t st) {
+    const size_t smem = (size_t)2 * XSH * 3 * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_stage_x<MODE, E, R2C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_stage_x<MODE, E, R2C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    k_stage_x<MODE, E, R2C><<<grid, 96, smem, st>>>(a, x.tw512, x.tw1024, mm, mt);
+}
+
+template <int MODE, bool R2C>
+static void launch_x2(bool exact, const StageArgs& a, const XStage& x, const CUtensorMap& mm,
+                      const CUtensorMap& mt, unsigned grid, cudaStream_t st) {
+    if (exact) launch_x1<MODE, true, R2C>(a, x, mm, mt, grid, st);
+    else launch_x1<MODE, false, R2C>(a, x, mm, mt, grid, st);
+}
+
+int launch_xstage(int mode, bool exact, const StageArgs& a0, const XStage& x, cudaStream_t st) {
+    StageArgs a = a0;
+    const long long rows = (long long)a.g.ny * a.g.nz;
+    const unsigned grid = (unsigned)(rows / 2);
+    // the plane-major slice [kx][row][3] as a 2-D float64 tensor (k_c2r_w's maps)
+    CUtensorMap mm{}, mt{};
+    const unsigned long long inner = (unsigned long long)rows * 6, pitch_b = (unsigned long long)x.blke * 16;
+    int rc;
+    if ((rc = make_map_2d_f64(&mm, x.X, inner, XSH, pitch_b, 12, 256)) ||
+        (rc = make_map_2d_f64(&mt, x.X, inner, XSH, pitch_b, 12, 1)))
+        return rc;
+    a.nparts = (int)grid;
+    switch (mode) {
+        case M_RK1: launch_x2<M_RK1, true>(exact, a, x, mm, mt, grid, st); break;
+        case M_RK2: launch_x2<M_RK2, true>(exact, a, x, mm, mt, grid, st); break;
+        case M_RK3: launch_x2<M_RK3, true>(exact, a, x, mm, mt, grid, st); break;
+        case M_RK4: launch_x2<M_RK4, false>(exact, a, x, mm, mt, grid, st); break;
+        default: set_error("x-row fused stage: RK4 stages only"); return MXB_EINVAL;
+    }
+    MXB_LAUNCH_CHECK();
+    if (mode == M_RK4) return launch_finalize(a, 0, st);
+    return MXB_OK;
 }
 
 }  // namespace mxb

@@ -90,4 +90,17 @@ int launch_partials(const StageArgs& a, double* out8, cudaStream_t st);
 int launch_commit(const StageArgs& a, const double* totals8, cudaStream_t st);
 Derived derive(const MatDev& m, const Grid& g);
 
+// x-row fused stage (stencil.cu k_stage_x): x c2r of the plane-major demag
+// spectra X -> stage update -> x r2c of the new state back into X (stages
+// 1-3), single rank, nx = 512.  X is [kx][row][3] with kx planes blke complex
+// elements apart; tw512 / tw1024 the length-512 / 1024 twiddle tables.
+struct XStage {
+    double2* X;
+    long long blke;
+    const double2* tw512;
+    const double2* tw1024;
+};
+bool xstage_eligible(const StageArgs& a);
+int launch_xstage(int mode, bool exact, const StageArgs& a, const XStage& x, cudaStream_t st);
+
 }  // namespace mxb

@@ -77,7 +77,7 @@
 #define MXB_PIPE_DISCARD_LATE 0
 #endif
 #ifndef MXB_PIPE_SIGNAL_REL     // completion signals as red.release instead of fence + atomicAdd
-#define MXB_PIPE_SIGNAL_REL 0
+#define MXB_PIPE_SIGNAL_REL 1
 #endif
 #ifndef MXB_PIPE_EARLY_READY // read the next unit's dependency counter during the current unit
 #define MXB_PIPE_EARLY_READY 0
@@ -89,7 +89,7 @@
 #define MXB_PIPE_LATE_SIGNAL 0
 #endif
 #ifndef MXB_PIPE_SIGNAL_EARLY   // signal the previous unit between this unit's TMA issue and its wait
-#define MXB_PIPE_SIGNAL_EARLY 0
+#define MXB_PIPE_SIGNAL_EARLY 1
 #endif
 #ifndef MXB_PIPE_NOBAR      // with the late signal: no CTA barrier after the staging wait
 #define MXB_PIPE_NOBAR 0
