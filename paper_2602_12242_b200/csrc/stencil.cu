@@ -1371,6 +1371,13 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
 // Results are bit-identical to the unfused kernels; the final stage's block
 // partials are reduced per row pair.
 // ---------------------------------------------------------------------------
+#ifndef MXB_XS_SWP   // k_stage_x: next cell's loads issued before this cell's arithmetic
+#define MXB_XS_SWP 0
+#endif
+#ifndef MXB_XS_PREFETCH   // k_stage_x: L2 prefetch of the stage rows during the c2r
+#define MXB_XS_PREFETCH 1
+#endif
+
 namespace mxb {
 namespace {
 constexpr int XSM = 512;        // complex FFT length of the x rows (px / 2)
@@ -1397,6 +1404,25 @@ k_stage_x(StageArgs a, const double2* __restrict__ tw512, const double2* __restr
         tma_load_2d(S + 512 * 6, &map_tail, xo0, 512, &mbar);
     }
     __syncthreads();   // mbarrier initialised before anyone polls it
+#if MXB_XS_PREFETCH
+    if (c == 0 && lane < 18) {
+        // the stage phase's rows into L2 while the c2r runs: the state rows
+        // r0 - 1 .. r0 + 2 and the pair's z +- 1 rows, and the pair's rows of
+        // the step-start state, K1 and S (one bulk prefetch per lane)
+        const Grid& g = a.g;
+        const long long R = (long long)g.ny * g.nz, N = g.N;
+        const int q = lane % 3, kind = lane / 3;
+        const double* base = nullptr;
+        long long r = row0, nr = 2;
+        if (kind == 0) { base = a.ys; r = row0 > 0 ? row0 - 1 : 0; nr = min(row0 + 3, R) - r; }
+        else if (kind == 1) { base = a.ys; r = row0 - g.ny; }
+        else if (kind == 2) { base = a.ys; r = row0 + g.ny; }
+        else if (kind == 3) base = a.y;
+        else if (kind == 4 && kK1) base = a.k1;
+        else if (kind == 5 && kS) base = a.s;
+        if (base && r >= 0 && r + nr <= R) prefetch_l2(base + q * N + r * XSM, (unsigned)(nr * XSM * 8));
+    }
+#endif
     double2 fa[16], fb[16], v[32];
     {
         double2 twp[16];
@@ -1438,49 +1464,72 @@ k_stage_x(StageArgs a, const double2* __restrict__ tw512, const double2* __restr
     const double* hd_s = reinterpret_cast<const double*>(S);   // [q][2048]: H_demag at [ln * 512 + x]
     double* out_s = reinterpret_cast<double*>(S) + 1024;       // [q][2048]: new state at [ln * 512 + x]
     double red[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int e = threadIdx.x; e < 2 * XSM; e += 96) {
+    // one cell's inputs (global loads; ghosts applied at compute)
+    struct In { double m[3], xp[3], xm[3], yp[3], ym[3], zp[3], zm[3], yv[3], k1v[3], sv[3]; };
+    auto load = [&](int e, In& u) {
+        const int ln = e >> 9, i = e & (XSM - 1);
+        const long long row = row0 + ln;
+        const int k = (int)(row / g.ny), j = (int)(row - (long long)k * g.ny);
+        const long long idx = row * XSM + i;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const long long o = q * N + idx;
+            u.m[q] = ld(a.ys, o);
+            u.xp[q] = i + 1 < XSM ? ld(a.ys, o + 1) : 0.0;
+            u.xm[q] = i > 0 ? ld(a.ys, o - 1) : 0.0;
+            u.yp[q] = j + 1 < g.ny ? ld(a.ys, o + XSM) : 0.0;
+            u.ym[q] = j > 0 ? ld(a.ys, o - XSM) : 0.0;
+            u.zp[q] = k + 1 < g.nz ? ld(a.ys, o + plane) : 0.0;
+            u.zm[q] = k > 0 ? ld(a.ys, o - plane) : 0.0;
+            u.yv[q] = ld(a.y, o);
+            u.k1v[q] = kK1 ? ld(a.k1, o) : 0.0;
+            u.sv[q] = kS ? a.s[o] : 0.0;
+        }
+    };
+    auto cell = [&](int e, In& u) {
         const int ln = e >> 9, i = e & (XSM - 1);
         const long long row = row0 + ln;
         const int k = (int)(row / g.ny), j = (int)(row - (long long)k * g.ny);
         const long long idx = row * XSM + i;
         const bool okxp = i + 1 < XSM, okxm = i > 0, okyp = j + 1 < g.ny, okym = j > 0;
         const bool zp_ok = k + 1 < g.nz, zm_ok = k > 0;
-        double m[3], xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
+        double hdv[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const long long o = q * N + idx;
-            m[q] = ld(a.ys, o);
-            xp[q] = okxp ? ld(a.ys, o + 1) : 0.0;
-            xm[q] = okxm ? ld(a.ys, o - 1) : 0.0;
-            yp[q] = okyp ? ld(a.ys, o + XSM) : 0.0;
-            ym[q] = okym ? ld(a.ys, o - XSM) : 0.0;
-            zp[q] = zp_ok ? ld(a.ys, o + plane) : 0.0;
-            zm[q] = zm_ok ? ld(a.ys, o - plane) : 0.0;
-        }
-        double yv[3], k1v[3], sv[3], hdv[3];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            yv[q] = ld(a.y, q * N + idx);
-            k1v[q] = kK1 ? ld(a.k1, q * N + idx) : 0.0;
-            sv[q] = kS ? a.s[q * N + idx] : 0.0;
-            hdv[q] = hd_s[q * 2048 + e];
-        }
-        if (!okxp) ghost_nb<E>(a, 0, +1, m, p, xp);
-        if (!okxm) ghost_nb<E>(a, 0, -1, m, p, xm);
-        if (!okyp) ghost_nb<E>(a, 1, +1, m, p, yp);
-        if (!okym) ghost_nb<E>(a, 1, -1, m, p, ym);
-        if (!zp_ok) ghost_nb<E>(a, 2, +1, m, p, zp);
-        if (!zm_ok) ghost_nb<E>(a, 2, -1, m, p, zm);
+        for (int q = 0; q < 3; ++q) hdv[q] = hd_s[q * 2048 + e];
+        if (!okxp) ghost_nb<E>(a, 0, +1, u.m, p, u.xp);
+        if (!okxm) ghost_nb<E>(a, 0, -1, u.m, p, u.xm);
+        if (!okyp) ghost_nb<E>(a, 1, +1, u.m, p, u.yp);
+        if (!okym) ghost_nb<E>(a, 1, -1, u.m, p, u.ym);
+        if (!zp_ok) ghost_nb<E>(a, 2, +1, u.m, p, u.zp);
+        if (!zm_ok) ghost_nb<E>(a, 2, -1, u.m, p, u.zm);
         double h[3], vn[3];
-        heff_nb<E, true>(a, a.ys, idx, i, j, k, m, cm, a.terms, xp, xm, yp, ym, zp, zm,
+        heff_nb<E, true>(a, a.ys, idx, i, j, k, u.m, cm, a.terms, u.xp, u.xm, u.yp, u.ym, u.zp, u.zm,
                          okxp ? hf : Af, okxm ? hf : Af, okyp ? hf : Af, okym ? hf : Af,
                          zp_ok ? hf : Af, zm_ok ? hf : Af, h, hdv);
-        stage_tail<MODE, E>(a, idx, cm, m, h, red, yv, kK1 ? k1v : nullptr, kS ? sv : nullptr, vn);
+        stage_tail<MODE, E>(a, idx, cm, u.m, h, red, u.yv, kK1 ? u.k1v : nullptr, kS ? u.sv : nullptr, vn);
         if (R2C) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) out_s[q * 2048 + e] = vn[q];
         }
+    };
+#if MXB_XS_SWP
+    // software pipelined: the next cell's loads are in flight during this cell's arithmetic
+    {
+        In cur, nxt;
+        load(threadIdx.x, cur);
+        for (int e = threadIdx.x; e < 2 * XSM; e += 96) {
+            if (e + 96 < 2 * XSM) load(e + 96, nxt);
+            cell(e, cur);
+            cur = nxt;
+        }
     }
+#else
+    for (int e = threadIdx.x; e < 2 * XSM; e += 96) {
+        In u;
+        load(e, u);
+        cell(e, u);
+    }
+#endif
     if (kFinal) {
         const bool is_max[4] = {false, false, false, true};
         block_reduce<4>(red, is_max);

@@ -2,7 +2,8 @@
 stage update -> x r2c of the new state, one kernel per RK4 stage) against
 the unfused kernels it replaces (k_c2r_w, k_stage_zt, k_r2c_w; MXB_XFUSE=0).
 
-Same arithmetic in the same order, so the state after a run is bit-identical;
+Same arithmetic in the same order as the TMA z-march stage kernel, so the
+state after a run is bit-identical where the unfused path runs that kernel;
 the <m> samples differ only in the order the per-block partial sums are
 added (the fused kernel reduces per row pair, the z-march per 32 x 4 x 64
 tile): <= 1e-15 relative.  The unfused path is itself pinned against the
@@ -58,30 +59,43 @@ def rand_m(g, seed):
     return m * (MS / np.sqrt((m * m).sum(axis=0)))
 
 
-def check_same(a, b):
+def zt_grid(g):
+    """The unfused path runs the TMA z-march stage kernel (heff_nb, the fused
+    kernel's arithmetic) when its 32 x 4 x 64 tiles fill the GPU; smaller
+    grids take the one-cell-per-thread kernel, whose exchange sum rounds
+    differently (<= 1e-13, test_full_size.py)."""
+    return -(-g.nx // 32) * -(-g.ny // 4) * -(-g.nz // 64) >= 4 * 148
+
+
+def check_same(a, b, bitwise):
     (ma, ta), (mb, tb) = a, b
-    assert np.array_equal(ma, mb), float(np.max(np.abs(ma - mb)) / MS)
+    if bitwise:
+        assert np.array_equal(ma, mb), float(np.max(np.abs(ma - mb)) / MS)
+        tol = 1e-15
+    else:
+        assert float(np.max(np.abs(ma - mb)) / MS) <= 1e-13
+        tol = 1e-13
     assert ta.shape == tb.shape
-    assert np.max(np.abs(ta - tb)) <= 1e-15 * max(1.0, float(np.max(np.abs(tb))))
+    assert np.max(np.abs(ta - tb)) <= tol * max(1.0, float(np.max(np.abs(tb))))
 
 
 MAT = dict(Ms=MS, A=1.3e-11, Ku=5e4, eK=(0.0, 0.0, 1.0), D=1e-3, alpha=0.1)
 
 
-@pytest.mark.parametrize("dims", [(16, 512, 512), (6, 37, 512), (1, 64, 512)],
-                         ids=["film16", "odd_ny_pairs_straddle_planes", "single_plane"])
+# (nx, ny, nz): the fused kernel takes nx = 512 x-rows; the plane pipeline ny = nz
+@pytest.mark.parametrize("dims", [(512, 128, 128), (512, 16, 16), (512, 8, 8)], ids=["n128", "n16", "n8"])
 def test_fused_stage_bitwise(dims):
     g = mx.GridSpec(*dims, 3e-9, 3e-9, 3e-9)
     mat = mx.MaterialMap(g, **MAT)
     kern = pipe_kernel(g)
     m0 = rand_m(g, 5)
-    check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}))
+    check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
 
 
 def test_fused_stage_time_dependent_bias_and_no_stage_renorm():
     """A bias that changes per stage (host stage-bias path, no graph replay)
     and the stage states left unnormalised."""
-    g = mx.GridSpec(8, 128, 512, 2e-9, 2.5e-9, 3e-9)
+    g = mx.GridSpec(512, 128, 128, 2e-9, 2.5e-9, 3e-9)
     mat = mx.MaterialMap(g, Ms=MS, A=1.3e-11, Ku=2e4, eK=(0.3, 0.0, 1.0), alpha=0.05)
 
     def bias(t):
@@ -90,29 +104,29 @@ def test_fused_stage_time_dependent_bias_and_no_stage_renorm():
     kern = pipe_kernel(g)
     m0 = rand_m(g, 6)
     kw = dict(bias=bias, renorm=False, exchange=True, anisotropy=True)
-    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw))
+    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
 
 
 def test_fused_stage_spatial_bias_field():
-    g = mx.GridSpec(4, 64, 512, 3e-9, 3e-9, 3e-9)
+    g = mx.GridSpec(512, 16, 16, 3e-9, 3e-9, 3e-9)
     mat = mx.MaterialMap(g, **MAT)
     field = np.random.default_rng(7).normal(size=(3,) + g.shape) * 1e4
     kern = pipe_kernel(g)
     m0 = rand_m(g, 8)
     kw = dict(bias=lambda t: field * (1.0 + 1e10 * t), exchange=True, dmi=True)
-    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw))
+    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
 
 
 def test_fused_stage_exact_mode():
     """numpy-rounding stage arithmetic (MXB_EXACT / set_exact): the fused kernel's E=true instance."""
-    g = mx.GridSpec(4, 64, 512, 3e-9, 3e-9, 3e-9)
+    g = mx.GridSpec(512, 128, 128, 3e-9, 3e-9, 3e-9)
     old = L.exact()
     L.set_exact(True)
     try:
         mat = mx.MaterialMap(g, **MAT)
         kern = pipe_kernel(g)
         m0 = rand_m(g, 9)
-        check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}))
+        check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
     finally:
         L.set_exact(old)
 
@@ -120,7 +134,7 @@ def test_fused_stage_exact_mode():
 def test_fused_stage_is_the_path_taken():
     """mxb_time_steps reports the launches of the path it ran: 10 per step fused
     (x forward, 4 x (pipeline + fused stage), finalize), 17 unfused."""
-    g = mx.GridSpec(16, 512, 512, 3e-9, 3e-9, 3e-9)
+    g = mx.GridSpec(512, 32, 32, 3e-9, 3e-9, 3e-9)
     mat = mx.MaterialMap(g, **MAT)
     kern = pipe_kernel(g)
     rhs = mx.PartitionedRHS(mat, exchange=True, anisotropy=True, dmi=True, demag=kern, bias=(1e4, 0, 0))
