@@ -1371,11 +1371,14 @@ int launch_energies(bool exact, const StageArgs& a, const double* m, const doubl
 // Results are bit-identical to the unfused kernels; the final stage's block
 // partials are reduced per row pair.
 // ---------------------------------------------------------------------------
+#ifndef MXB_XS_PAIR   // k_stage_x: two x-adjacent cells per thread iteration, 16-byte loads
+#define MXB_XS_PAIR 0
+#endif
 #ifndef MXB_XS_SWP   // k_stage_x: next cell's loads issued before this cell's arithmetic
 #define MXB_XS_SWP 0
 #endif
 #ifndef MXB_XS_PREFETCH   // k_stage_x: L2 prefetch of the stage rows during the c2r
-#define MXB_XS_PREFETCH 1
+#define MXB_XS_PREFETCH 0
 #endif
 
 namespace mxb {
@@ -1512,7 +1515,43 @@ k_stage_x(StageArgs a, const double2* __restrict__ tw512, const double2* __restr
             for (int q = 0; q < 3; ++q) out_s[q * 2048 + e] = vn[q];
         }
     };
-#if MXB_XS_SWP
+#if MXB_XS_PAIR
+    // two x-adjacent cells per iteration: 16-byte loads of the pair's values (the
+    // x neighbours inside the pair come from the pair itself)
+    for (int pp = threadIdx.x; pp < XSM; pp += 96) {
+        const int e0 = 2 * pp;
+        const int ln = e0 >> 9, i0 = e0 & (XSM - 1);
+        const long long row = row0 + ln;
+        const int k = (int)(row / g.ny), j = (int)(row - (long long)k * g.ny);
+        const long long idx0 = row * XSM + i0;
+        In u0, u1;
+        auto ld2 = [&](const double* b, long long o) {
+            return __ldg(reinterpret_cast<const double2*>(b + o));
+        };
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const long long o = q * N + idx0;
+            const double2 mm = ld2(a.ys, o);
+            u0.m[q] = mm.x; u1.m[q] = mm.y;
+            u0.xp[q] = mm.y; u1.xm[q] = mm.x;
+            u0.xm[q] = i0 > 0 ? ld(a.ys, o - 1) : 0.0;
+            u1.xp[q] = i0 + 2 < XSM ? ld(a.ys, o + 2) : 0.0;
+            const double2 yp2 = j + 1 < g.ny ? ld2(a.ys, o + XSM) : make_double2(0.0, 0.0);
+            const double2 ym2 = j > 0 ? ld2(a.ys, o - XSM) : make_double2(0.0, 0.0);
+            const double2 zp2 = k + 1 < g.nz ? ld2(a.ys, o + plane) : make_double2(0.0, 0.0);
+            const double2 zm2 = k > 0 ? ld2(a.ys, o - plane) : make_double2(0.0, 0.0);
+            const double2 y2 = ld2(a.y, o);
+            const double2 k12 = kK1 ? ld2(a.k1, o) : make_double2(0.0, 0.0);
+            const double2 s2 = kS ? *reinterpret_cast<const double2*>(a.s + o) : make_double2(0.0, 0.0);
+            u0.yp[q] = yp2.x; u1.yp[q] = yp2.y; u0.ym[q] = ym2.x; u1.ym[q] = ym2.y;
+            u0.zp[q] = zp2.x; u1.zp[q] = zp2.y; u0.zm[q] = zm2.x; u1.zm[q] = zm2.y;
+            u0.yv[q] = y2.x; u1.yv[q] = y2.y; u0.k1v[q] = k12.x; u1.k1v[q] = k12.y;
+            u0.sv[q] = s2.x; u1.sv[q] = s2.y;
+        }
+        cell(e0, u0);
+        cell(e0 + 1, u1);
+    }
+#elif MXB_XS_SWP
     // software pipelined: the next cell's loads are in flight during this cell's arithmetic
     {
         In cur, nxt;
@@ -1598,8 +1637,10 @@ k_stage_x(StageArgs a, const double2* __restrict__ tw512, const double2* __restr
 }
 
 bool xstage_eligible(const StageArgs& a) {
-    const char* e = getenv("MXB_XFUSE");   // read per call: tests switch it
-    if (e && e[0] == '0') return false;
+    // opt-in (MXB_XFUSE=1): measured slower than the unfused kernels at 512^3
+    // (DESIGN.md section 4); read per call, tests switch it
+    const char* e = getenv("MXB_XFUSE");
+    if (!e || e[0] != '1') return false;
     const Grid& g = a.g;
     return a.mat.uniform && a.mat.all_magnetic && a.ghost != MXB_GHOST_PERIODIC &&
            !(a.terms & (MXB_TERM_CUBIC | MXB_TERM_BULK_DMI)) && (a.terms & MXB_TERM_DEMAG) &&

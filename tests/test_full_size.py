@@ -9,8 +9,8 @@ through size-independent properties of the hot path.
     mirror-symmetric in x, y and z: <= 1e-12 of Ms
   * the plane pipeline (default) against the 5-pass path: <= 1e-14 normwise
   * two RK4 steps of the bench problem (demag + exchange + DMI + anisotropy +
-    Zeeman): |m| = Ms within 4 ulp; the x-row fused stages against the unfused
-    kernels: bit-identical; against the register z-march stage kernel:
+    Zeeman): |m| = Ms within 4 ulp; the opt-in x-row fused stages against the
+    default kernels: bit-identical; against the register z-march stage kernel:
     <= 1e-13 normwise; <m> traces <= 1e-12
 """
 import os
@@ -107,11 +107,11 @@ def test_full_size_steps(method):
 
     m_t, tr_t = run({})
     assert np.max(np.abs(np.sqrt(np.einsum("cijk,cijk->ijk", m_t, m_t)) - MS)) <= 4 * np.spacing(MS)
-    # the x-row fused stages (default here) against the unfused kernels: bit-identical state
-    m_u, tr_u = run({"MXB_XFUSE": "0"})
+    # the opt-in x-row fused stages against the default unfused kernels: bit-identical state
+    m_u, tr_u = run({"MXB_XFUSE": "1"})
     assert np.array_equal(m_t, m_u)
     assert np.max(np.abs(tr_t - tr_u)) <= 1e-15 * MS
-    # ... and the unfused path with the TMA z-march stage kernel off (k_stage_zm)
-    m_c, tr_c = run({"MXB_XFUSE": "0", "MXB_ZTMA": "0"})
+    # ... and the TMA z-march stage kernel off (k_stage_zm)
+    m_c, tr_c = run({"MXB_ZTMA": "0"})
     assert nrm(m_t, m_c) <= 1e-13
     assert np.max(np.abs(tr_t - tr_c)) <= 1e-12

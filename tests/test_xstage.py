@@ -1,6 +1,7 @@
-"""The x-row fused stage (stencil.cu k_stage_x: x c2r of the demag spectra ->
-stage update -> x r2c of the new state, one kernel per RK4 stage) against
-the unfused kernels it replaces (k_c2r_w, k_stage_zt, k_r2c_w; MXB_XFUSE=0).
+"""The x-row fused stage (stencil.cu k_stage_x, opt-in MXB_XFUSE=1: x c2r of
+the demag spectra -> stage update -> x r2c of the new state, one kernel per
+RK4 stage) against the unfused kernels it replaces (k_c2r_w, k_stage_zt,
+k_r2c_w; the default path).
 
 Same arithmetic in the same order as the TMA z-march stage kernel, so the
 state after a run is bit-identical where the unfused path runs that kernel;
@@ -89,7 +90,7 @@ def test_fused_stage_bitwise(dims):
     mat = mx.MaterialMap(g, **MAT)
     kern = pipe_kernel(g)
     m0 = rand_m(g, 5)
-    check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
+    check_same(run(g, mat, kern, m0, {"MXB_XFUSE": "1"}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
 
 
 def test_fused_stage_time_dependent_bias_and_no_stage_renorm():
@@ -104,7 +105,7 @@ def test_fused_stage_time_dependent_bias_and_no_stage_renorm():
     kern = pipe_kernel(g)
     m0 = rand_m(g, 6)
     kw = dict(bias=bias, renorm=False, exchange=True, anisotropy=True)
-    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
+    check_same(run(g, mat, kern, m0, {"MXB_XFUSE": "1"}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
 
 
 def test_fused_stage_spatial_bias_field():
@@ -114,7 +115,7 @@ def test_fused_stage_spatial_bias_field():
     kern = pipe_kernel(g)
     m0 = rand_m(g, 8)
     kw = dict(bias=lambda t: field * (1.0 + 1e10 * t), exchange=True, dmi=True)
-    check_same(run(g, mat, kern, m0, {}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
+    check_same(run(g, mat, kern, m0, {"MXB_XFUSE": "1"}, **kw), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}, **kw), zt_grid(g))
 
 
 def test_fused_stage_exact_mode():
@@ -126,7 +127,7 @@ def test_fused_stage_exact_mode():
         mat = mx.MaterialMap(g, **MAT)
         kern = pipe_kernel(g)
         m0 = rand_m(g, 9)
-        check_same(run(g, mat, kern, m0, {}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
+        check_same(run(g, mat, kern, m0, {"MXB_XFUSE": "1"}), run(g, mat, kern, m0, {"MXB_XFUSE": "0"}), zt_grid(g))
     finally:
         L.set_exact(old)
 
@@ -152,5 +153,5 @@ def test_fused_stage_is_the_path_taken():
             return nl.value
         return with_env(env, f)
 
-    assert launches({}) == 2 * 10
-    assert launches({"MXB_XFUSE": "0"}) == 2 * 17
+    assert launches({"MXB_XFUSE": "1"}) == 2 * 10
+    assert launches({}) == 2 * 17
