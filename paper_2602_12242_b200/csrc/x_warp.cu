@@ -38,6 +38,13 @@ using namespace ff;
 #define MXB_XW_TWPRE 1
 #endif
 
+#ifndef MXB_XW_R2C_DIRECT   // plane-major r2c: outputs stored from registers instead of TMA boxes
+#define MXB_XW_R2C_DIRECT 0
+#endif
+#ifndef MXB_XW_PFD_DEFAULT   // x passes: L2 prefetch of the input pfd CTAs ahead (0 = off)
+#define MXB_XW_PFD_DEFAULT 0
+#endif
+
 namespace {
 constexpr int XM = 512;          // complex FFT length (px / 2)
 constexpr int XHX = XM + 1;      // spectrum bins kept (px / 2 + 1)
@@ -48,7 +55,7 @@ __global__ void __launch_bounds__(96, 4)
 k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __restrict__ out, int CHP,
         long long BLKE, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
         const int* __restrict__ halt, const __grid_constant__ CUtensorMap map_main,
-        const __grid_constant__ CUtensorMap map_tail) {
+        const __grid_constant__ CUtensorMap map_tail, int pfd) {
     if (halt && *halt) return;
     // 3 x 1024 transpose tiles, then the output pair: [kx][line][c] (plane-major,
     // TMA boxes of 256 planes x 96 B) or [line][kx][c] (row-major, two bulk rows)
@@ -66,6 +73,11 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
         mbar_expect(&mbar, 3 * 2 * XM * 8);
         for (int q = 0; q < 3; ++q)
             bulk_g2s_tx(W + q * XM, in + q * cstride + row0 * pitch, 2 * XM * 8, &mbar);
+        // the input of the CTA pfd row pairs ahead (about one wave later on this
+        // SM slot) into L2, so its staging wait is an L2 hit
+        if (pfd && blockIdx.x + pfd < gridDim.x)
+            for (int q = 0; q < 3; ++q)
+                prefetch_l2(in + q * cstride + (row0 + 2LL * pfd) * pitch, 2 * XM * 8);
     }
     __syncthreads();
     mbar_wait(&mbar, 0);
@@ -128,6 +140,20 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
             }
         }
     }
+#if MXB_XW_R2C_DIRECT
+    if (PM) {
+        // straight from registers: lane kx's 16 bytes of each line at X[kx][row][c]
+        // (the pair's 96-byte run per plane is completed in L2 by the three warps)
+#pragma unroll
+        for (int ln = 0; ln < 2; ++ln)
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int kx = lane + 32 * i;
+                if (kx < XHX) out[(long long)kx * BLKE + (row0 + ln) * 3 + c] = xo[ln][i];
+            }
+        return;
+    }
+#endif
     __syncthreads();   // every warp is done with its tile: stage the output pair
 #pragma unroll
     for (int ln = 0; ln < 2; ++ln)
@@ -166,7 +192,7 @@ __global__ void __launch_bounds__(96, 4)
 k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restrict__ out, long long cstride,
         int pitch, const double2* __restrict__ tw512, const double2* __restrict__ tw1024,
         const int* __restrict__ halt, const __grid_constant__ CUtensorMap map_main,
-        const __grid_constant__ CUtensorMap map_tail) {
+        const __grid_constant__ CUtensorMap map_tail, int pfd) {
     if (halt && *halt) return;
     // the input pair ([kx][line][c] by TMA boxes, or [line][kx][c] by two bulk
     // rows), then 3 x 1024 transpose tiles
@@ -182,6 +208,12 @@ k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restri
             tma_load_2d(S, &map_main, x, 0, &mbar);
             tma_load_2d(S + 256 * 6, &map_main, x, 256, &mbar);
             tma_load_2d(S + 512 * 6, &map_tail, x, 512, &mbar);
+            if (pfd && blockIdx.x + pfd < gridDim.x) {   // the spectra slice pfd CTAs ahead into L2
+                const int xn = (int)((row0 + 2LL * pfd) * 6);
+                tma_prefetch_2d(&map_main, xn, 0);
+                tma_prefetch_2d(&map_main, xn, 256);
+                tma_prefetch_2d(&map_tail, xn, 512);
+            }
         } else {
             mbar_expect(&mbar, 2 * XHX * 48);
             bulk_g2s_tx(S, X + row0 * CHP * 3, XHX * 48, &mbar);
@@ -234,6 +266,9 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
     const bool on = !(xe && xe[0] == '0');
     if (!on || M != XM || nhalf != XM / 2 || (nrows & 1) || pitch != XM) return -1;
     const bool pm = CH == 1;
+    // L2 prefetch distance in CTAs (MXB_XW_PFD, read per launch; 0 = off)
+    const char* pe = getenv("MXB_XW_PFD");
+    const int pfd = pe ? atoi(pe) : MXB_XW_PFD_DEFAULT;
     if (!pm && CH < XHX) return -1;   // row-major only for a single rank
     const unsigned grid = (unsigned)(nrows / 2);
     const size_t smem_r2c = (size_t)2 * XHX * 3 * sizeof(double2);   // >= the tiles
@@ -258,11 +293,11 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
             return MXB_ECUDA;
     }
     if (fwd) {
-        if (pm) k_r2c_w<true><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt);
-        else k_r2c_w<false><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt);
+        if (pm) k_r2c_w<true><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt, pfd);
+        else k_r2c_w<false><<<grid, 96, smem_r2c, st>>>(in_r, cstride, pitch, X, CHP, BLKE, twM, tw2M, halt, mm, mt, pfd);
     } else {
-        if (pm) k_c2r_w<true><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt);
-        else k_c2r_w<false><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt);
+        if (pm) k_c2r_w<true><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt, pfd);
+        else k_c2r_w<false><<<grid, 96, smem_c2r, st>>>(X, CHP, BLKE, out_r, cstride, pitch, twM, tw2M, halt, mm, mt, pfd);
     }
     MXB_LAUNCH_CHECK();
     return MXB_OK;
