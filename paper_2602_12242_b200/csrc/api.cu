@@ -929,7 +929,7 @@ int mxb_state_energies(mxb_ctx* c, mxb_demag* d, const mxb_terms* t, const mxb_b
 // part of a captured step's key, so a cached graph never replays another path
 static double env_sig() {
     uint64_t h = 1469598103934665603ull;
-    for (const char* n : {"MXB_XFUSE", "MXB_ZTMA", "MXB_XWARP", "MXB_XW_PFD"}) {
+    for (const char* n : {"MXB_XFUSE", "MXB_ZTMA", "MXB_XWARP", "MXB_XW_PFD", "MXB_XW_PFD_C2R"}) {
         const char* v = getenv(n);
         for (const char* q = v ? v : "\x01"; *q; ++q) h = (h ^ (unsigned char)*q) * 1099511628211ull;
         h = (h ^ 0xffu) * 1099511628211ull;

@@ -38,11 +38,8 @@ using namespace ff;
 #define MXB_XW_TWPRE 1
 #endif
 
-#ifndef MXB_XW_R2C_DIRECT   // plane-major r2c: outputs stored from registers instead of TMA boxes
-#define MXB_XW_R2C_DIRECT 0
-#endif
-#ifndef MXB_XW_PFD_DEFAULT   // x passes: L2 prefetch of the input pfd CTAs ahead (0 = off)
-#define MXB_XW_PFD_DEFAULT 0
+#ifndef MXB_XW_PFD_DEFAULT   // r2c: L2 prefetch of the input pfd CTAs ahead (296: 8.3 -> 7.9 ms per step)
+#define MXB_XW_PFD_DEFAULT 296
 #endif
 
 namespace {
@@ -140,20 +137,6 @@ k_r2c_w(const double* __restrict__ in, long long cstride, int pitch, double2* __
             }
         }
     }
-#if MXB_XW_R2C_DIRECT
-    if (PM) {
-        // straight from registers: lane kx's 16 bytes of each line at X[kx][row][c]
-        // (the pair's 96-byte run per plane is completed in L2 by the three warps)
-#pragma unroll
-        for (int ln = 0; ln < 2; ++ln)
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                const int kx = lane + 32 * i;
-                if (kx < XHX) out[(long long)kx * BLKE + (row0 + ln) * 3 + c] = xo[ln][i];
-            }
-        return;
-    }
-#endif
     __syncthreads();   // every warp is done with its tile: stage the output pair
 #pragma unroll
     for (int ln = 0; ln < 2; ++ln)
@@ -266,9 +249,11 @@ int warp_rows(bool fwd, int M, const double* in_r, double2* X, double* out_r, lo
     const bool on = !(xe && xe[0] == '0');
     if (!on || M != XM || nhalf != XM / 2 || (nrows & 1) || pitch != XM) return -1;
     const bool pm = CH == 1;
-    // L2 prefetch distance in CTAs (MXB_XW_PFD, read per launch; 0 = off)
-    const char* pe = getenv("MXB_XW_PFD");
-    const int pfd = pe ? atoi(pe) : MXB_XW_PFD_DEFAULT;
+    // r2c: L2 prefetch of the input rows pfd CTAs ahead (MXB_XW_PFD, read per launch;
+    // 0 = off); c2r: of its spectrum slice by tensor prefetch (MXB_XW_PFD_C2R, off:
+    // measured 70% slower)
+    const char* pe = getenv(fwd ? "MXB_XW_PFD" : "MXB_XW_PFD_C2R");
+    const int pfd = pe ? atoi(pe) : (fwd ? MXB_XW_PFD_DEFAULT : 0);
     if (!pm && CH < XHX) return -1;   // row-major only for a single rank
     const unsigned grid = (unsigned)(nrows / 2);
     const size_t smem_r2c = (size_t)2 * XHX * 3 * sizeof(double2);   // >= the tiles

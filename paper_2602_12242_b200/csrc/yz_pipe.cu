@@ -85,6 +85,9 @@
 #ifndef MXB_PIPE_PF_NEXT     // L2 prefetch of the next A unit's XP row once its ticket is known
 #define MXB_PIPE_PF_NEXT 0
 #endif
+#ifndef MXB_PIPE_PF_DIST     // ... of the A unit MXB_PIPE_PF_DIST tickets after the next (0: the next)
+#define MXB_PIPE_PF_DIST 0
+#endif
 #ifndef MXB_PIPE_LATE_SIGNAL   // signal the previous unit mid-unit (after the next ticket), not before compute
 #define MXB_PIPE_LATE_SIGNAL 0
 #endif
@@ -581,7 +584,7 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     // thread 0, once the next ticket is known: an A unit's XP row comes from
     // DRAM -- start pulling it into L2 while this unit finishes
     auto prefetch_next_a = [&](long long t) {
-        const Unit nu = tmap(t);
+        const Unit nu = tmap(t + MXB_PIPE_PF_DIST);
         if (nu.kind == U_A)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
                              a.XP + xp_row(a, plane_xp, nu.plane, nu.idx, N * 3)),
