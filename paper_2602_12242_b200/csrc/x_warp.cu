@@ -38,8 +38,8 @@ using namespace ff;
 #define MXB_XW_TWPRE 1
 #endif
 
-#ifndef MXB_XW_PFD_DEFAULT   // r2c: L2 prefetch of the input pfd CTAs ahead (296: 8.3 -> 7.9 ms per step)
-#define MXB_XW_PFD_DEFAULT 296
+#ifndef MXB_XW_PFD_DEFAULT   // r2c: L2 prefetch of the input pfd CTAs ahead (148: 8.23 -> 7.71 ms per step)
+#define MXB_XW_PFD_DEFAULT 148
 #endif
 
 namespace {
