@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
 #ifndef MXB_ZT_MINB   // CTAs per SM the TMA z-march is compiled for (register budget)
 #define MXB_ZT_MINB (16 / MXB_ZTY)
 #endif
+#ifndef MXB_ZT_YDEDUP   // TMA z-march: no step-start-state box when it is the stage state
+#define MXB_ZT_YDEDUP 1
+#endif
 #ifndef MXB_ZM_CTAS
 #define MXB_ZM_CTAS 3
 #endif
@@ -856,7 +859,7 @@ template <int MODE> struct ZtAux {
 
 template <int MODE, bool E>
 __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a, const __grid_constant__ ZtMaps maps,
-                                                            int nfields, int has_hd) {
+                                                            int nfields, int has_hd, int y_is_ys) {
     if (a.halt && *(volatile const int*)a.halt) return;
     constexpr bool kFinal = MODE == M_RK4 || MODE == M_EULER;
     // state box (doubles): the x origin of a TMA box must be 16-byte aligned,
@@ -954,7 +957,14 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a
                 for (int q = 0; q < 3; ++q) v[q] = ab[ff * APL + (q * ZTY + ty) * ZTX + tx];
             };
             if (has_hd) A3(f++, hdv);
-            if (ZtAux<MODE>::kY) A3(f++, yv);
+            if (ZtAux<MODE>::kY) {
+                if (y_is_ys) {   // first stage: the step-start state is the stage state (no aux box)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) yv[q] = m[q];
+                } else {
+                    A3(f++, yv);
+                }
+            }
             if (ZtAux<MODE>::kK1) A3(f++, k1v);
             if (ZtAux<MODE>::kS) A3(f++, sv);
             double h[3];
@@ -1029,7 +1039,10 @@ static bool launch_zt(const StageArgs& a, cudaStream_t st) {
     int nf = 0;
     const int has_hd = (a.terms & MXB_TERM_DEMAG) && a.hd ? 1 : 0;
     if (has_hd && field_map(&mp.aux[nf++], a.hd, a.g, ZTX, ZTY)) return false;
-    if (ZtAux<MODE>::kY && field_map(&mp.aux[nf++], a.y, a.g, ZTX, ZTY)) return false;
+    // the first stage (and Euler) read the step-start state as the stage state:
+    // its values come from the state ring, not a second TMA box of the same data
+    const int y_is_ys = MXB_ZT_YDEDUP && a.y == a.ys ? 1 : 0;
+    if (ZtAux<MODE>::kY && !y_is_ys && field_map(&mp.aux[nf++], a.y, a.g, ZTX, ZTY)) return false;
     if (ZtAux<MODE>::kK1 && field_map(&mp.aux[nf++], a.k1, a.g, ZTX, ZTY)) return false;
     if (ZtAux<MODE>::kS && field_map(&mp.aux[nf++], a.s, a.g, ZTX, ZTY)) return false;
     const size_t smem = (size_t)(4 * ((3 * (ZTY + 2) * (ZTX + 4) + 15) / 16 * 16) + 2 * nf * 3 * ZTY * ZTX) * sizeof(double);
@@ -1038,7 +1051,7 @@ static bool launch_zt(const StageArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(k_stage_zt<MODE, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
-    k_stage_zt<MODE, E><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd);
+    k_stage_zt<MODE, E><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd, y_is_ys);
     return true;
 }
 
