@@ -38,9 +38,6 @@ using namespace ff;
 #define MXB_XW_TWPRE 1
 #endif
 
-#ifndef MXB_XW_C2R_PF_LINES   // c2r prefetch (MXB_XW_PFD_C2R) by L2 line prefetches instead of TMA
-#define MXB_XW_C2R_PF_LINES 0
-#endif
 #ifndef MXB_XW_PFD_DEFAULT   // r2c: L2 prefetch of the input pfd CTAs ahead (148: 8.23 -> 7.71 ms per step)
 #define MXB_XW_PFD_DEFAULT 148
 #endif
@@ -194,32 +191,18 @@ k_c2r_w(const double2* __restrict__ X, int CHP, long long BLKE, double* __restri
             tma_load_2d(S, &map_main, x, 0, &mbar);
             tma_load_2d(S + 256 * 6, &map_main, x, 256, &mbar);
             tma_load_2d(S + 512 * 6, &map_tail, x, 512, &mbar);
-#if !MXB_XW_C2R_PF_LINES
             if (pfd && blockIdx.x + pfd < gridDim.x) {   // the spectra slice pfd CTAs ahead into L2
                 const int xn = (int)((row0 + 2LL * pfd) * 6);
                 tma_prefetch_2d(&map_main, xn, 0);
                 tma_prefetch_2d(&map_main, xn, 256);
                 tma_prefetch_2d(&map_tail, xn, 512);
             }
-#endif
         } else {
             mbar_expect(&mbar, 2 * XHX * 48);
             bulk_g2s_tx(S, X + row0 * CHP * 3, XHX * 48, &mbar);
             bulk_g2s_tx(S + XHX * 3, X + (row0 + 1) * CHP * 3, XHX * 48, &mbar);
         }
     }
-#if MXB_XW_C2R_PF_LINES
-    if (PM && pfd && blockIdx.x + pfd < gridDim.x) {
-        // the slice of the CTA pfd row pairs ahead: 513 runs of 96 B, one per kx
-        // plane, as per-thread L2 line prefetches (LSU, not the TMA unit)
-        const double2* nb = X + (row0 + 2LL * pfd) * 3;
-        for (int kx = threadIdx.x; kx < XHX; kx += 96) {
-            const char* p0 = reinterpret_cast<const char*>(nb + (long long)kx * BLKE);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 95));
-        }
-    }
-#endif
     __syncthreads();   // mbarrier initialised before anyone polls it
 #if MXB_XW_TWPRE
     // the untangling twiddles do not depend on the spectra: load them while the
