@@ -100,6 +100,12 @@
 #ifndef MXB_PIPE_KPRE       // B: first kernel entry loaded before the spectrum store + barrier
 #define MXB_PIPE_KPRE 0
 #endif
+#ifndef MXB_PIPE_KPF_L1     // B multiply: L1 prefetch of the kernel entry this many iterations ahead
+#define MXB_PIPE_KPF_L1 0
+#endif
+#ifndef MXB_PIPE_KROT       // B multiply: kernel entries loaded this many iterations ahead (0 = off)
+#define MXB_PIPE_KROT 0
+#endif
 #ifndef MXB_PIPE_SEEN       // skip re-acquiring a plane counter this CTA already saw complete
 #define MXB_PIPE_SEEN 0
 #endif
@@ -861,12 +867,56 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
 #if MXB_PIPE_KPAIR
                 // kz and L - kz share the parity-reduced entry kz' = min(kz, L - kz):
                 // each entry is loaded once and applied to both (sign flip of XZ, YZ)
+#if MXB_PIPE_KROT
+                // kernel entries rotated through registers: the loads of the entry
+                // MXB_PIPE_KROT iterations ahead are in flight during this one's updates
+                constexpr int KD = MXB_PIPE_KROT;
+                double2 kq[KD][3];
+                {
+                    const int q0 = a.cplx ? L : (int)threadIdx.x;
+#pragma unroll
+                    for (int d = 0; d < KD; ++d) {
+                        const int qd = q0 + 96 * d;
+                        if (qd <= L / 2) {
+                            const double2* kr = krow + qd * 3;
+#if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                            kq[d][0] = ldg_hint(kr, pk); kq[d][1] = ldg_hint(kr + 1, pk); kq[d][2] = ldg_hint(kr + 2, pk);
+#else
+                            kq[d][0] = __ldg(kr); kq[d][1] = __ldg(kr + 1); kq[d][2] = __ldg(kr + 2);
+#endif
+                        }
+                    }
+                }
+#endif
 #if MXB_PIPE_KUNROLL > 1
 #pragma unroll(kKUnroll)
 #endif
                 for (int q = a.cplx ? L : threadIdx.x; q <= L / 2; q += 96) {
                     const double2* kr = krow + q * 3;
-#if MXB_PIPE_KPRE
+#if MXB_PIPE_KPF_L1
+                    // the entry MXB_PIPE_KPF_L1 iterations ahead into L1 (no registers held)
+                    if (q + 96 * MXB_PIPE_KPF_L1 <= L / 2) {
+                        const char* pn = reinterpret_cast<const char*>(kr + 96 * MXB_PIPE_KPF_L1 * 3);
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn));
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(pn + 47));
+                    }
+#endif
+#if MXB_PIPE_KROT
+                    const double2 q01 = kq[0][0], q23 = kq[0][1], q45 = kq[0][2];
+#pragma unroll
+                    for (int d = 0; d + 1 < KD; ++d) {
+                        kq[d][0] = kq[d + 1][0]; kq[d][1] = kq[d + 1][1]; kq[d][2] = kq[d + 1][2];
+                    }
+                    if (q + 96 * KD <= L / 2) {
+                        const double2* kn = kr + 96 * KD * 3;
+#if MXB_PIPE_HINTS && MXB_PIPE_HINT_K
+                        kq[KD - 1][0] = ldg_hint(kn, pk); kq[KD - 1][1] = ldg_hint(kn + 1, pk);
+                        kq[KD - 1][2] = ldg_hint(kn + 2, pk);
+#else
+                        kq[KD - 1][0] = __ldg(kn); kq[KD - 1][1] = __ldg(kn + 1); kq[KD - 1][2] = __ldg(kn + 2);
+#endif
+                    }
+#elif MXB_PIPE_KPRE
                     double2 q01, q23, q45;
                     if (q == (int)threadIdx.x) {
                         q01 = pre01; q23 = pre23; q45 = pre45;
