@@ -101,7 +101,7 @@
 #define MXB_PIPE_KPRE 0
 #endif
 #ifndef MXB_PIPE_KPF_L1     // B multiply: L1 prefetch of the kernel entry this many iterations ahead
-#define MXB_PIPE_KPF_L1 2
+#define MXB_PIPE_KPF_L1 0
 #endif
 #ifndef MXB_PIPE_KROT       // B multiply: kernel entries loaded this many iterations ahead (0 = off)
 #define MXB_PIPE_KROT 0
