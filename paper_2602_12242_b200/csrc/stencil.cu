@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* ctl, const double* parti
 #ifndef MXB_ZT_MINB   // CTAs per SM the TMA z-march is compiled for (register budget)
 #define MXB_ZT_MINB (16 / MXB_ZTY)
 #endif
+#ifndef MXB_ZT_DEEP   // TMA z-march: state 3 / aux 2 planes ahead for stages with <= 2 aux fields
+#define MXB_ZT_DEEP 0
+#endif
 #ifndef MXB_ZT_YDEDUP   // TMA z-march: no step-start-state box when it is the stage state
 #define MXB_ZT_YDEDUP 1
 #endif
@@ -857,7 +860,9 @@ template <int MODE> struct ZtAux {
     static constexpr bool kY = MODE >= M_RK1, kK1 = MODE == M_RK4, kS = MODE == M_RK3 || MODE == M_RK4;
 };
 
-template <int MODE, bool E>
+// SD: state planes issued ahead of the one being waited for (ring of SD + 2
+// slots: planes k-1, k, k+1 in use), AD: aux planes issued ahead (AD + 1 slots)
+template <int MODE, bool E, int SD, int AD>
 __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a, const __grid_constant__ ZtMaps maps,
                                                             int nfields, int has_hd, int y_is_ys) {
     if (a.halt && *(volatile const int*)a.halt) return;
@@ -867,10 +872,11 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a
     constexpr int SX = ZTX + 4, SY = ZTY + 2, SBOX = 3 * SY * SX;
     constexpr int SPL = (SBOX + 15) / 16 * 16;                          // slot stride: 128-byte aligned
     constexpr int APL = 3 * ZTY * ZTX;                              // one aux field plane
+    constexpr int NS = SD + 2, NA = AD + 1;
     extern __shared__ __align__(128) double zsm[];
-    double* stp = zsm;                       // [4][3][SY][SX]
-    double* aux = zsm + 4 * SPL;             // [2][nfields][3][ZTY][ZTX]
-    __shared__ alignas(8) unsigned long long mst[4], max_[2];
+    double* stp = zsm;                       // [NS][3][SY][SX]
+    double* aux = zsm + NS * SPL;            // [NA][nfields][3][ZTY][ZTX]
+    __shared__ alignas(8) unsigned long long mst[NS], max_[NA];
     const Grid& g = a.g;
     const long long plane = (long long)g.nx * g.ny;
     const int tx = threadIdx.x & (ZTX - 1), ty = threadIdx.x / ZTX;
@@ -883,49 +889,46 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a
     double red[4] = {0.0, 0.0, 0.0, 0.0};
     const unsigned st_bytes = SBOX * 8, aux_bytes = nfields * APL * 8;
 
+    // plane kk's state slot and phase: n = kk - k0 + 1 (plane k0 - 1 is n = 0), slot
+    // n % NS, phase (n / NS) & 1; aux: n = kk - k0, slot n % NA
+    auto sslot = [&](int kk) { return (kk - k0 + 1) % NS; };
+    auto aslot = [&](int kk) { return (kk - k0) % NA; };
     auto issue_state = [&](int kk) {   // thread 0
-        unsigned long long* mb = &mst[(kk + 4) & 3];
+        unsigned long long* mb = &mst[sslot(kk)];
         mbar_expect(mb, st_bytes);
-        tma_load_4d(stp + ((kk + 4) & 3) * SPL, &maps.st, i0 - 2, j0 - 1, kk, 0, mb);
+        tma_load_4d(stp + sslot(kk) * SPL, &maps.st, i0 - 2, j0 - 1, kk, 0, mb);
     };
     auto issue_aux = [&](int kk) {     // thread 0
-        unsigned long long* mb = &max_[kk & 1];
+        unsigned long long* mb = &max_[aslot(kk)];
         mbar_expect(mb, aux_bytes);
         for (int f = 0; f < nfields; ++f)
-            tma_load_4d(aux + ((kk & 1) * nfields + f) * APL, &maps.aux[f], i0, j0, kk, 0, mb);
+            tma_load_4d(aux + (aslot(kk) * nfields + f) * APL, &maps.aux[f], i0, j0, kk, 0, mb);
     };
     if (threadIdx.x == 0) {
-        for (int q = 0; q < 4; ++q) mbar_init(&mst[q]);
-        mbar_init(&max_[0]);
-        mbar_init(&max_[1]);
-        issue_state(k0 - 1);
-        issue_state(k0);
-        issue_state(k0 + 1);
-        if (nfields) issue_aux(k0);
+        for (int q = 0; q < NS; ++q) mbar_init(&mst[q]);
+        for (int q = 0; q < NA; ++q) mbar_init(&max_[q]);
+        for (int kk = k0 - 1; kk < k0 + SD && kk <= k1; ++kk) issue_state(kk);
+        if (nfields)
+            for (int kk = k0; kk < k0 + AD && kk < k1; ++kk) issue_aux(kk);
     }
     __syncthreads();
-    unsigned sph = 0, aph = 0;   // phase bit per slot
     auto wait_state = [&](int kk) {
-        const int sl = (kk + 4) & 3;
-        mbar_wait(&mst[sl], (sph >> sl) & 1u);
-        sph ^= 1u << sl;
+        const int n = kk - k0 + 1;
+        mbar_wait(&mst[n % NS], (unsigned)(n / NS) & 1u);
     };
     wait_state(k0 - 1);
     wait_state(k0);
     for (int k = k0; k < k1; ++k) {
         if (threadIdx.x == 0) {
-            if (k + 2 <= k1) issue_state(k + 2);          // slot of plane k - 2
-            if (nfields && k + 1 < k1) issue_aux(k + 1);  // slot of plane k - 1
+            if (k + SD <= k1) issue_state(k + SD);           // slot of plane k - 2
+            if (nfields && k + AD < k1) issue_aux(k + AD);   // slot of plane k - 1
         }
         wait_state(k + 1);
-        if (nfields) {
-            mbar_wait(&max_[k & 1], (aph >> (k & 1)) & 1u);
-            aph ^= 1u << (k & 1);
-        }
+        if (nfields) mbar_wait(&max_[aslot(k)], (unsigned)((k - k0) / NA) & 1u);
         if (in) {
-            const double* sc = stp + ((k + 4) & 3) * SPL;
-            const double* sp = stp + ((k + 5) & 3) * SPL;
-            const double* sm1 = stp + ((k + 3) & 3) * SPL;
+            const double* sc = stp + sslot(k) * SPL;
+            const double* sp = stp + sslot(k + 1) * SPL;
+            const double* sm1 = stp + sslot(k - 1) * SPL;
             auto S = [&](const double* b, int q, int yy, int xx) { return b[(q * SY + yy) * SX + xx]; };
             const long long idx = (long long)k * plane + col;
             double m[3], xp[3], xm[3], yp[3], ym[3], zp[3], zm[3];
@@ -949,7 +952,7 @@ __global__ void __launch_bounds__(ZTX * ZTY, MXB_ZT_MINB) k_stage_zt(StageArgs a
             if (!zp_ok) ghost_nb<E>(a, 2, +1, m, p, zp);
             if (!zm_ok) ghost_nb<E>(a, 2, -1, m, p, zm);
             // aux fields in the order hd (if any), y, k1, s
-            const double* ab = aux + (k & 1) * nfields * APL;
+            const double* ab = aux + aslot(k) * nfields * APL;
             double hdv[3], yv[3], k1v[3], sv[3];
             int f = 0;
             auto A3 = [&](int ff, double v[3]) {
@@ -1045,13 +1048,19 @@ static bool launch_zt(const StageArgs& a, cudaStream_t st) {
     if (ZtAux<MODE>::kY && !y_is_ys && field_map(&mp.aux[nf++], a.y, a.g, ZTX, ZTY)) return false;
     if (ZtAux<MODE>::kK1 && field_map(&mp.aux[nf++], a.k1, a.g, ZTX, ZTY)) return false;
     if (ZtAux<MODE>::kS && field_map(&mp.aux[nf++], a.s, a.g, ZTX, ZTY)) return false;
-    const size_t smem = (size_t)(4 * ((3 * (ZTY + 2) * (ZTX + 4) + 15) / 16 * 16) + 2 * nf * 3 * ZTY * ZTX) * sizeof(double);
+    // deeper rings for the stages with few aux fields (their bytes in flight per
+    // CTA are otherwise the smallest): MXB_ZT_DEEP
+    const bool deep = MXB_ZT_DEEP && nf <= 2;
+    const int NS = deep ? 5 : 4, NA = deep ? 3 : 2;
+    const size_t smem = (size_t)(NS * ((3 * (ZTY + 2) * (ZTX + 4) + 15) / 16 * 16) + NA * nf * 3 * ZTY * ZTX) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_stage_zt<MODE, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_stage_zt<MODE, E, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_stage_zt<MODE, E, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
-    k_stage_zt<MODE, E><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd, y_is_ys);
+    if (deep) k_stage_zt<MODE, E, 3, 2><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd, y_is_ys);
+    else k_stage_zt<MODE, E, 2, 1><<<zm_grid(a.g), ZTX * ZTY, smem, st>>>(a, mp, nf, has_hd, y_is_ys);
     return true;
 }
 
