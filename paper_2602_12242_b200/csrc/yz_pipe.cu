@@ -106,6 +106,9 @@
 #ifndef MXB_PIPE_KROT       // B multiply: kernel entries loaded this many iterations ahead (0 = off)
 #define MXB_PIPE_KROT 0
 #endif
+#ifndef MXB_PIPE_EARLY_ACQ  // next ticket + acquire of its dependency during this unit's staging wait
+#define MXB_PIPE_EARLY_ACQ 0
+#endif
 #ifndef MXB_PIPE_SEEN       // skip re-acquiring a plane counter this CTA already saw complete
 #define MXB_PIPE_SEEN 0
 #endif
@@ -313,13 +316,15 @@ struct Sched {
     // per-plane counters only grow and that acquire already ordered this CTA's
     // later reads after every producer, so further B / C units of the same
     // plane skip the load
+    // acquired (thread 0): u's counter was already read with an acquire and showed
+    // the target (MXB_PIPE_EARLY_ACQ) -- nothing to wait for, ordering established
     __device__ bool wait_ready(const Unit& u, int* flag, Unit& pending, unsigned early = 0u,
-                               int* seen = nullptr) const {
+                               int* seen = nullptr, bool acquired = false) const {
         if (threadIdx.x == 0) {
             *flag = 1;
             const unsigned* c;
             unsigned tg;
-            bool need = dep(u, &c, &tg);
+            bool need = dep(u, &c, &tg) && !acquired;
             if (need && seen && ((u.kind == U_B && seen[0] == u.plane) || (u.kind == U_C && seen[1] == u.plane)))
                 need = false;
             if (need && early >= tg) {
@@ -740,6 +745,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
     }
     __syncthreads();
     Unit cur = tmap(next_ticket);
+#if MXB_PIPE_EARLY_ACQ
+    bool early_ok = false;   // thread 0: cur's dependency already acquired as complete
+#endif
     // completion of the previous unit is signalled after this unit's staging
     // wait (its stores have drained by then), or before blocking
     Unit pending{U_NONE, 0, 0};
@@ -750,6 +758,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         early = 0u;
 #elif MXB_PIPE_SEEN
         if (!sc.wait_ready(cur, &flag, pending, 0u, seen)) return;
+#elif MXB_PIPE_EARLY_ACQ
+        if (!sc.wait_ready(cur, &flag, pending, 0u, nullptr, early_ok)) return;
+        early_ok = false;
 #else
         if (!sc.wait_ready(cur, &flag, pending)) return;
 #endif
@@ -765,6 +776,17 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             }
             sc.signal(pending);
             pending.kind = U_NONE;
+        }
+#endif
+#if MXB_PIPE_EARLY_ACQ
+        // thread 0, while this unit's input is in flight: the next ticket, and an
+        // acquire read of its dependency counter (both latencies overlap the
+        // staging wait instead of the FFT and the next unit's start); a single
+        // read, never a blocking wait
+        if (threadIdx.x == 0) {
+            next_ticket = atomicAdd(sc.ticket(), 1u);
+            const Unit nu = tmap(next_ticket);
+            early_ok = nu.kind != U_NONE && sc.ready(nu);
         }
 #endif
         stage_wait(cur);
@@ -810,7 +832,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
         if (cur.kind != U_C) {
             fw::fft1024<-1, MXB_HALF_IN != 0>(v, Wc, lane, tw);
             if (threadIdx.x == 0) {
+#if !MXB_PIPE_EARLY_ACQ
                 next_ticket = atomicAdd(sc.ticket(), 1u);
+#endif
 #if MXB_PIPE_PF_NEXT
                 prefetch_next_a(next_ticket);
 #endif
@@ -994,7 +1018,9 @@ k_yz_pipe_w(PipeArgs a, const double2* __restrict__ tw, const int* __restrict__ 
             if (cur.kind == U_C) {
                 // ---- y inverse of row z = idx -> XP row (n of L kept)
                 if (threadIdx.x == 0) {
+#if !MXB_PIPE_EARLY_ACQ
                     next_ticket = atomicAdd(sc.ticket(), 1u);
+#endif
 #if MXB_PIPE_PF_NEXT
                     prefetch_next_a(next_ticket);
 #endif
